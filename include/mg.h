@@ -1,0 +1,131 @@
+/*
+ * include/mg.h -- C ABI of the B200-native MarginGate decode engine.
+ *
+ * Paper: arxiv 2605.30218 "MarginGate".  One call
+ * of mg_decode_step is one MarginGate decode step (PAPER.md:185-217,
+ * Fig. fig:margingate_arch):
+ *   BF16 batched fast forward that tentatively appends the K/V column
+ *    -> fused top-1/top-2 margin g = l(1) - l(2)
+ *    -> gate  protected && g < tau
+ *   -> deterministic verifier on the gated rows ->
+ *   fast / verified / repair commit of the single current column
+ *    -> r_verify / r_repair accounting.
+ *
+ * Conventions:
+ *  - Every entry point returns mg_status; nothing throws or aborts across the
+ *    ABI.  MG_ERR_INVALID and MG_ERR_CAPACITY leave the context unchanged.
+ *    MG_ERR_CUDA is sticky: the context is dead, only mg_destroy is legal.
+ *  - Ownership: the caller allocates the four device buffers reported by
+ *    mg_query_sizes (e.g. with torch) and keeps them alive until mg_destroy.
+ *    The context owns host metadata, CUDA events and tensor maps.
+ *  - Synchrony: all work is ordered on the stream given to mg_init.
+ *    mg_decode_step returns once the step is enqueued; it synchronises
+ *    internally only to read the gate's trigger count when a protected row
+ *    exists and 0 < tau (the verifier's token count is data dependent).
+ *    Device outputs are valid after stream completion.  mg_stats synchronises.
+ *  - Threading: one context = one host thread.  Not thread-safe.
+ *  - Arrays whose name ends in _host are host memory, _dev device memory.
+ */
+#ifndef MG_H
+#define MG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MG_OK = 0,
+  MG_ERR_INVALID = 1,   /* bad argument; no state change                       */
+  MG_ERR_CAPACITY = 2,  /* position would reach max_seq / pages exhausted      */
+  MG_ERR_CUDA = 3,      /* CUDA error; sticky, context unusable                */
+  MG_ERR_STATE = 4,     /* call not legal in this state (e.g. slot inactive)   */
+  MG_ERR_NUMERIC = 5    /* a logit was NaN (reported by mg_stats)              */
+} mg_status;
+
+typedef struct mg_ctx mg_ctx; /* opaque */
+
+/* Model shape + capacity.  Shapes of the named models: SURVEY.md 2.3
+ * [public cfg]; init of weights: DESIGN.md 3.1 (counter PRNG, weight_seed). */
+typedef struct {
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab, qkv_bias;
+  float rms_eps, rope_theta;
+  uint64_t weight_seed;
+  int32_t max_batch;   /* rows per decode step, 1..256                         */
+  int32_t max_slots;   /* concurrent requests                                  */
+  int32_t max_seq;     /* positions per request (prompt + decode)              */
+  int32_t page_size;   /* K/V page size in tokens (16, 32 or 64)               */
+  int32_t verify_chunk;/* max tokens per verifier/prefill launch (0: 512)       */
+} mg_config;
+
+/* Bytes of each caller-owned device buffer (256-byte aligned). */
+typedef struct {
+  size_t weights, kv_fast, kv_shadow, workspace;
+} mg_sizes;
+
+typedef struct {
+  void *weights, *kv_fast, *kv_shadow, *workspace;
+} mg_buffers;
+
+/* Device-side counters, summed over all steps since mg_init.
+ * r_verify = triggers / protected_rows, r_repair = repairs / protected_rows
+ * (PAPER.md:215). */
+typedef struct {
+  uint64_t steps, rows, protected_rows, triggers, verified, repairs, verifier_launches, catchup_tokens;
+  uint32_t error_flags; /* bit0: NaN logit seen */
+} mg_stats_t;
+
+/* Sizes the four buffers for `cfg`.  MG_ERR_INVALID on unsupported shapes
+ * (d_model % 64, d_ff % 64, (H+2KV)*hd % 128, vocab % 128, head_dim in
+ * {64,128}, H % KV). */
+mg_status mg_query_sizes(const mg_config* cfg, mg_sizes* out);
+
+/* Creates a context on the current CUDA device, generates the weights into
+ * bufs->weights and captures nothing else.  `cuda_stream` is
+ * a cudaStream_t (NULL = legacy default stream). */
+mg_status mg_init(const mg_config* cfg, const mg_buffers* bufs, void* cuda_stream, mg_ctx** out);
+
+/* Deterministic prefill of request `slot`: runs the pinned
+ * verifier schedule over prompt_host[0..len) into the shadow cache, copies the
+ * columns into the fast cache and writes the first token (argmax, not gated)
+ * to *first_token_host.  Synchronises.  The slot becomes active.
+ * MG_ERR_STATE if the slot is already active; MG_ERR_CAPACITY if len+1 >
+ * max_seq or pages run out; MG_ERR_INVALID for len < 1 or token ids out of
+ * range. */
+mg_status mg_prefill(mg_ctx* ctx, int32_t slot, const int32_t* prompt_host, int32_t len,
+                     int32_t* first_token_host);
+
+/* One MarginGate decode step over `batch` active, distinct slots.
+ *   slots_host[b]          request of row b
+ *   protected_host[b]      1 = the row is gated; NULL = all rows
+ *   threshold              tau >= 0; 0 = pure BF16 (r_verify = 0), +INFINITY =
+ *                          always-on verification (r_verify = 1)
+ *   tokens_out_dev[b]      committed token (int32)
+ *   kind_out_dev[b]        nullable: 0 fast, 1 verified, 2 repair
+ *   margin_out_dev[b]      nullable: fp32 margin g of the fast logits
+ * Each row consumes its last committed token at position p and commits exactly
+ * one token.  MG_ERR_INVALID: batch not in [1, max_batch], inactive or
+ * duplicate slot, tau NaN or < 0.  MG_ERR_CAPACITY: a row's p + 1 would reach
+ * max_seq. */
+mg_status mg_decode_step(mg_ctx* ctx, const int32_t* slots_host, int32_t batch, const uint8_t* protected_host,
+                         float threshold, int32_t* tokens_out_dev, uint8_t* kind_out_dev, float* margin_out_dev);
+
+/* Synchronises the stream and copies the counters; returns MG_ERR_NUMERIC if
+ * a NaN logit was seen (counters still written). */
+mg_status mg_stats(mg_ctx* ctx, mg_stats_t* out_host);
+
+/* Frees the slot's pages; the slot may be prefilled again. */
+mg_status mg_release(mg_ctx* ctx, int32_t slot);
+
+void mg_destroy(mg_ctx* ctx);
+
+/* Last error message of this context (or of the last failed mg_init when
+ * ctx == NULL).  Valid until the next call on the context. */
+const char* mg_last_error(const mg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

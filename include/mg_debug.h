@@ -1,0 +1,97 @@
+/*
+ * include/mg_debug.h -- TEST-ONLY op-level entry points of libmargingate.so.
+ *
+ * Not part of the product ABI.  They launch exactly the kernels the engine
+ * launches (same code, same schedules) on caller-provided device buffers, so
+ * the parity tests can compare each hot-path kernel with the oracle on
+ * identical inputs (SURVEY 8(c) "Parity protocol" step 1), plus hooks to read
+ * engine state.  All pointers are DEVICE pointers unless suffixed _host; all
+ * work is enqueued on `stream` (cudaStream_t, NULL = default) and the call
+ * returns after enqueueing (no synchronisation).  bf16 tensors are uint16_t
+ * bit patterns, row-major.  Return: MG_OK or MG_ERR_INVALID / MG_ERR_CUDA.
+ */
+#ifndef MG_DEBUG_H
+#define MG_DEBUG_H
+
+#include "mg.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* K0: DESIGN.md 3.1 generator for ONE logical tensor (kind 0..3) into out[n]. */
+mg_status mgd_gen_tensor(uint64_t seed, uint32_t tensor_id, int64_t n, int32_t kind, int32_t fan_in,
+                         uint16_t* out, void* stream);
+
+/* a2: out[T][d] = bf16((x*inv)*w), inv = 1/sqrtf(sum x^2/d + eps), fixed tree. */
+mg_status mgd_rmsnorm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t d, float eps, uint16_t* out,
+                      void* stream);
+
+/* GEMM partials: out[s][t][n] = sum_{k in split s} x[t][k] * W[n][k].
+ * impl 0 = tcgen05 (TMA + TMEM), 1 = CUDA-core small-T kernel.
+ * splits = split-K count over 64-wide k-blocks; mma_n = tcgen05 instruction N
+ * (16 = the verifier's pinned slot groups, 0 = whole tile); tile_n = tokens
+ * per CTA (16..256, multiple of 16; 0 = auto).  N % 128 == 0, K % 64 == 0. */
+mg_status mgd_gemm(const uint16_t* x, const uint16_t* W, int32_t T, int32_t N, int32_t K, int32_t splits,
+                   int32_t impl, int32_t mma_n, int32_t tile_n, float* out, void* stream);
+
+/* QKV epilogue: acc = sum_s part[s][t][:] (+bias) -> RoPE(q,k) -> q[T][H*hd],
+ * k[T][KV*hd], v[T][KV*hd] (dense outputs, not the paged cache). */
+mg_status mgd_qkv_epilogue(const float* part, int32_t splits, const uint16_t* bias, const int32_t* pos,
+                           int32_t T, int32_t H, int32_t KV, int32_t hd, float theta, int32_t max_pos,
+                           uint16_t* q, uint16_t* k, uint16_t* v, void* stream);
+
+/* Decode attention over a dense per-token K/V:
+ * q[T][H*hd]; K,V [T][KV][key_stride][hd]; n_keys[T]; keys cut in `chunk`-key
+ * chunks (combined in chunk order) -> o[T][H*hd]. */
+mg_status mgd_attention(const uint16_t* q, const uint16_t* K, const uint16_t* V, const int32_t* n_keys, int32_t T,
+                        int32_t H, int32_t KV, int32_t hd, int32_t key_stride, int32_t chunk, uint16_t* o,
+                        void* stream);
+
+/* out[t][i] = bf16(x[t][i] + sum_s part[s][t][i]) */
+mg_status mgd_residual(const uint16_t* x, const float* part, int32_t splits, int32_t T, int32_t N, uint16_t* out,
+                       void* stream);
+
+/* a[t][j] = bf16(silu(g) * u), g/u from the interleaved-by-64 gate/up layout
+ * of part[s][t][2*F] (physical row r: tile r/128, gate if r%128 < 64). */
+mg_status mgd_swiglu(const float* part, int32_t splits, int32_t T, int32_t F, uint16_t* out, void* stream);
+
+/* Top-2 under (value desc, id asc): v1,i1,v2,i2,g per row of logits[T][V];
+ * *nan_flag (device int) |= 1 on NaN. */
+mg_status mgd_top2(const float* logits, int32_t T, int32_t V, float* v1, int32_t* i1, float* v2, int32_t* i2,
+                   float* g, int32_t* nan_flag, void* stream);
+
+/* Gate: trig[b] = prot[b] && g[b] < tau; rows[0..n) ascending; n -> *count. */
+mg_status mgd_gate(const float* g, const uint8_t* prot, int32_t B, float tau, uint8_t* trig, int32_t* rows,
+                   int32_t* count, void* stream);
+
+/* ---- engine introspection (synchronise; host outputs) ---- */
+/* Fast (which=0) or shadow (which=1) column (slot, pos) -> out [L][2][KV][hd] */
+mg_status mgd_read_column(mg_ctx* ctx, int32_t which, int32_t slot, int32_t pos, uint16_t* out_host);
+/* FNV-1a digest of a whole cache (all active slots, all written positions),
+ * excluding (skip_slot, skip_pos) if skip_slot >= 0. */
+mg_status mgd_cache_digest(mg_ctx* ctx, int32_t which, int32_t skip_slot, int32_t skip_pos, uint64_t* out_host);
+/* Per-row debug record of the LAST decode step: f_tok, g, v1, v2, trig,
+ * v_tok (-1), v_g, kind, out (each [B]). */
+mg_status mgd_last_step(mg_ctx* ctx, int32_t* f_tok, float* g, float* v1, float* v2, uint8_t* trig,
+                        int32_t* v_tok, float* v_g, uint8_t* kind, int32_t* out);
+/* Capture the fp32 fast logits [B][V] of subsequent steps into dev_buf (NULL: off). */
+mg_status mgd_capture_logits(mg_ctx* ctx, float* dev_buf);
+/* Copy the weight tensor (layer, which) as the ORACLE's logical layout
+ * (DESIGN.md 3.1 ids) to out_dev. */
+mg_status mgd_weight(mg_ctx* ctx, int32_t layer, int32_t which, uint16_t* out_dev, int64_t* n_host);
+/* Schedule in force for a T-token launch: writes splits of qkv,o,gu,down,lm,
+ * attention chunk, gemm impl, mma_n (8 ints) for det (det=1) or fast (det=0). */
+mg_status mgd_schedule(mg_ctx* ctx, int32_t T, int32_t det, int32_t max_ctx, int32_t* out8_host);
+/* Kernel launches enqueued by this context since init (the bench's
+ * gpu_launches claim). */
+mg_status mgd_launch_count(mg_ctx* ctx, uint64_t* out_host);
+/* Per-kernel-class event timing of subsequent steps (1 on / 0 off); read back
+ * average ms per launch of the GEMM class and the whole step. */
+mg_status mgd_set_timing(mg_ctx* ctx, int32_t on);
+mg_status mgd_timing(mg_ctx* ctx, double* out8_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -86,7 +86,7 @@ def lib():
                 "or_model_tensor": (u16p, [C.c_void_p, C.c_int32, C.c_int32, _P(C.c_int64)]),
                 "or_state_create": (C.c_void_p, [C.c_void_p, C.c_int32, C.c_int32]),
                 "or_state_free": (None, [C.c_void_p]),
-                "or_prefill": (C.c_int32, [C.c_void_p, C.c_int32, i32p, C.c_int32, _P(Sched)]),
+                "or_prefill": (C.c_int32, [C.c_void_p, C.c_int32, i32p, C.c_int32, _P(Sched), f32p]),
                 "or_step": (C.c_int32, [C.c_void_p, i32p, C.c_int32, u8p, C.c_float, _P(Sched), _P(Sched),
                                         u8p, i32p, u8p, i32p, f32p, f32p, f32p, u8p, i32p, f32p, u8p, i32p,
                                         f32p]),
@@ -292,9 +292,11 @@ class State:
         self.n_rows, self.max_seq = n_rows, max_seq
         self._h = lib().or_state_create(model._h, n_rows, max_seq)
 
-    def prefill(self, row: int, prompt, det: Sched) -> int:
+    def prefill(self, row: int, prompt, det: Sched, want_logits: bool = False):
         p = np.ascontiguousarray(prompt, dtype=np.int32)
-        return int(lib().or_prefill(self._h, row, i32(p), p.size, C.byref(det)))
+        lg = np.empty(self.model.shape["vocab"], np.float32) if want_logits else None
+        y0 = int(lib().or_prefill(self._h, row, i32(p), p.size, C.byref(det), f32(lg)))
+        return (y0, lg) if want_logits else y0
 
     def step(self, rows, prot, tau, fast: Sched, det: Sched, forced_trig=None, forced_out=None,
              forced_kind=None, want_logits=False):

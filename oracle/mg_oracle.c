@@ -451,7 +451,8 @@ static void copy_column(or_state* s, int32_t from, int32_t to, int32_t row, int3
       }
 }
 
-int32_t or_prefill(or_state* s, int32_t row, const int32_t* prompt, int32_t len, const or_sched* det) {
+int32_t or_prefill(or_state* s, int32_t row, const int32_t* prompt, int32_t len, const or_sched* det,
+                   float* logits_out) {
   const or_cfg* c = &s->m->c;
   float* logits = (float*)malloc(sizeof(float) * (size_t)c->vocab);
   int32_t* h = s->hist + (int64_t)row * (s->max_seq + 1);
@@ -463,6 +464,7 @@ int32_t or_prefill(or_state* s, int32_t row, const int32_t* prompt, int32_t len,
   float v1, v2, g; int32_t i1, i2, nan = 0;
   or_top2(logits, 1, c->vocab, &v1, &i1, &v2, &i2, &g, &nan);
   if (nan) s->stats[8] += 1;
+  if (logits_out) memcpy(logits_out, logits, sizeof(float) * (size_t)c->vocab);
   h[len] = i1;
   s->pos[row] = len;
   s->shadow_len[row] = len;

@@ -91,7 +91,8 @@ void      or_state_free(or_state* s);
 
 /* deterministic prefill of `row`: fills the shadow cache
  * with the det schedule, copies it into the fast cache, returns y0. */
-int32_t or_prefill(or_state* s, int32_t row, const int32_t* prompt, int32_t len, const or_sched* det);
+int32_t or_prefill(or_state* s, int32_t row, const int32_t* prompt, int32_t len, const or_sched* det,
+                   float* logits_out /* nullable [V]: logits at position len-1 */);
 
 /* One MarginGate decode step over rows[0..B) (SURVEY 8(c)
  * step 3).  Outputs per batch position b (all nullable except out_tok):

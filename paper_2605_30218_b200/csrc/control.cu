@@ -1,0 +1,298 @@
+// control.cu -- margin, gate, verifier bookkeeping and commit
+// (SURVEY 8(a) rows a8 (top-2), a9, a10 bookkeeping, a11).
+//
+// k_top2_partial / k_top2_final: top-1/top-2 of fp32 logits under the total
+// order (value desc, id asc) -- exact, so any merge order gives the same
+// (v1,i1,v2,i2); g = v1 - v2 is one IEEE subtraction.
+// k_gate: trig = prot && g < tau, ballot/popc
+// compaction in ascending row order, catch-up token list of every gated row
+// (positions shadow_len..p, A1).
+// k_commit: fast / verified / repair: a repair copies the
+// verifier's column p of every layer (K and V) from the shadow cache into
+// the fast cache and emits the verifier token; nothing else is written.
+#include <climits>
+
+#include "common.cuh"
+#include "control.h"
+#include "kernels.h"
+
+namespace mg {
+
+struct Top2 {
+  float v1;
+  int i1;
+  float v2;
+  int i2;
+};
+
+__device__ __forceinline__ bool better(float a, int ia, float b, int ib) { return a > b || (a == b && ia < ib); }
+
+__device__ __forceinline__ void t2_push(Top2& t, float v, int i) {
+  if (better(v, i, t.v1, t.i1)) {
+    t.v2 = t.v1;
+    t.i2 = t.i1;
+    t.v1 = v;
+    t.i1 = i;
+  } else if (better(v, i, t.v2, t.i2)) {
+    t.v2 = v;
+    t.i2 = i;
+  }
+}
+// merge two top-2 sets over disjoint index ranges
+__device__ __forceinline__ Top2 t2_merge(const Top2& a, const Top2& b) {
+  Top2 r;
+  if (better(a.v1, a.i1, b.v1, b.i1)) {
+    r.v1 = a.v1; r.i1 = a.i1;
+    if (better(a.v2, a.i2, b.v1, b.i1)) { r.v2 = a.v2; r.i2 = a.i2; } else { r.v2 = b.v1; r.i2 = b.i1; }
+  } else {
+    r.v1 = b.v1; r.i1 = b.i1;
+    if (better(a.v1, a.i1, b.v2, b.i2)) { r.v2 = a.v1; r.i2 = a.i1; } else { r.v2 = b.v2; r.i2 = b.i2; }
+  }
+  return r;
+}
+__device__ __forceinline__ Top2 t2_shfl(const Top2& t, int off) {
+  Top2 o;
+  o.v1 = __shfl_xor_sync(0xffffffffu, t.v1, off);
+  o.i1 = __shfl_xor_sync(0xffffffffu, t.i1, off);
+  o.v2 = __shfl_xor_sync(0xffffffffu, t.v2, off);
+  o.i2 = __shfl_xor_sync(0xffffffffu, t.i2, off);
+  return o;
+}
+
+int top2_blocks(int V) {
+  int nb = (V + 8191) / 8192;
+  return nb < 1 ? 1 : (nb > 64 ? 64 : nb);
+}
+
+// grid (T, nb), 256 threads; block b scans [b*V/nb, (b+1)*V/nb)
+__global__ void __launch_bounds__(256) k_top2_partial(const float* __restrict__ logits, int V, int nb,
+                                                      float* __restrict__ part, int32_t* __restrict__ nan_flag) {
+  __shared__ Top2 sm[8];
+  const int t = blockIdx.x, b = blockIdx.y;
+  const int lo = chunk_start(V, nb, b), hi = chunk_start(V, nb, b + 1);
+  const float* l = logits + (size_t)t * V;
+  Top2 r{-INFINITY, INT_MAX, -INFINITY, INT_MAX};
+  bool nan = false;
+  for (int j = lo + threadIdx.x; j < hi; j += 256) {
+    float v = l[j];
+    if (v != v) { nan = true; v = -INFINITY; }
+    t2_push(r, v, j);
+  }
+  if (nan) atomicOr(nan_flag, 1);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) r = t2_merge(r, t2_shfl(r, off));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = r;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Top2 a = sm[0];
+    for (int w = 1; w < 8; ++w) a = t2_merge(a, sm[w]);
+    float* p = part + ((size_t)t * nb + b) * 4;
+    p[0] = a.v1; p[1] = __int_as_float(a.i1); p[2] = a.v2; p[3] = __int_as_float(a.i2);
+  }
+}
+
+__global__ void k_top2_final(const float* __restrict__ part, int nb, float* v1, int32_t* i1, float* v2,
+                             int32_t* i2, float* g) {
+  const int t = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  const float* p = part + (size_t)t * nb * 4;
+  Top2 a{p[0], __float_as_int(p[1]), p[2], __float_as_int(p[3])};
+  for (int b = 1; b < nb; ++b) {
+    const float* q = p + b * 4;
+    a = t2_merge(a, Top2{q[0], __float_as_int(q[1]), q[2], __float_as_int(q[3])});
+  }
+  if (v1) v1[t] = a.v1;
+  if (i1) i1[t] = a.i1;
+  if (v2) v2[t] = a.v2;
+  if (i2) i2[t] = a.i2;
+  if (g) g[t] = __fsub_rn(a.v1, a.v2);
+}
+
+cudaError_t launch_top2(const float* logits, int T, int V, float* part, int nb, float* v1, int32_t* i1, float* v2,
+                        int32_t* i2, float* g, int32_t* nan_flag, cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  dim3 g1(T, nb);
+  k_top2_partial<<<g1, 256, 0, st>>>(logits, V, nb, part, nan_flag);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_top2_final<<<T, 32, 0, st>>>(part, nb, v1, i1, v2, i2, g);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ gate
+// Single CTA of 1024 threads (B <= 1024).  Row b = thread b.
+__global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
+  __shared__ int wsum[32], wgap[32];
+  const int b = threadIdx.x, warp = b >> 5, lane = b & 31;
+  const bool valid = b < a.B;
+  int slot = 0, p = 0, s0 = 0;
+  bool tr = false;
+  if (valid) {
+    slot = a.slots[b];
+    p = a.pos[slot];
+    s0 = a.shadow_len[slot];
+    const bool prot = a.prot ? a.prot[b] != 0 : true;
+    tr = prot && (a.g[b] < a.tau);  // strict <
+  }
+  const int gap = tr ? (p - s0 + 1) : 0;
+  // exclusive scans of trig flags and gaps (ascending row order)
+  const unsigned bal = __ballot_sync(0xffffffffu, tr);
+  int rank_in_warp = __popc(bal & ((1u << lane) - 1u));
+  int g_incl = gap;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, g_incl, off);
+    if (lane >= off) g_incl += v;
+  }
+  if (lane == 31) { wsum[warp] = __popc(bal); wgap[warp] = g_incl; }
+  __syncthreads();
+  if (b == 0) {
+    int acc = 0, accg = 0;
+    for (int w = 0; w < 32; ++w) {
+      const int c = wsum[w], cg = wgap[w];
+      wsum[w] = acc; wgap[w] = accg;
+      acc += c; accg += cg;
+    }
+    a.ctrl[0] = acc;   // number of gated rows
+    a.ctrl[1] = accg;  // catch-up tokens M
+  }
+  __syncthreads();
+  if (!valid) return;
+  a.trig[b] = tr ? 1 : 0;
+  if (!tr) { a.rank[b] = -1; return; }
+  const int r = wsum[warp] + rank_in_warp;
+  const int off = wgap[warp] + g_incl - gap;
+  a.rank[b] = r;
+  a.ctrl[2 + r] = b;
+  a.last[r] = off + gap - 1;
+  const int32_t* h = a.hist + (size_t)slot * a.hist_stride;
+  for (int q = s0; q <= p; ++q) {
+    const int e = off + (q - s0);
+    a.cu_slot[e] = slot;
+    a.cu_pos[e] = q;
+    a.cu_tok[e] = h[q];
+    a.cu_nk[e] = q + 1;
+  }
+}
+
+cudaError_t launch_gate(const GateArgs& a, cudaStream_t st) {
+  if (a.B > 1024) return cudaErrorInvalidValue;
+  k_gate<<<1, 1024, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ prepare
+// fast-path token list: slot, position p = pos[slot], input token hist[slot][p]
+__global__ void k_prepare(const int32_t* __restrict__ slots, int B, const int32_t* __restrict__ pos,
+                          const int32_t* __restrict__ hist, int hist_stride, int32_t* f_slot, int32_t* f_pos,
+                          int32_t* f_tok, int32_t* f_nk) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int s = slots[b], p = pos[s];
+  f_slot[b] = s;
+  f_pos[b] = p;
+  f_tok[b] = hist[(size_t)s * hist_stride + p];
+  f_nk[b] = p + 1;
+}
+
+cudaError_t launch_prepare(const int32_t* slots, int B, const int32_t* pos, const int32_t* hist, int hist_stride,
+                           int32_t* f_slot, int32_t* f_pos, int32_t* f_tok, int32_t* f_nk, cudaStream_t st) {
+  k_prepare<<<(B + 127) / 128, 128, 0, st>>>(slots, B, pos, hist, hist_stride, f_slot, f_pos, f_tok, f_nk);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ column copy
+// copy columns [p0, p1) of `slot`, all layers, K and V, src pool -> dst pool
+__device__ __forceinline__ void copy_cols(const ColCopy& c, int slot, int p0, int p1, int tid, int nth) {
+  const int vec_per_col = c.hd / 8;
+  const int per_pos = c.L * 2 * c.kv * vec_per_col;
+  const int total = (p1 - p0) * per_pos;
+  for (int e = tid; e < total; e += nth) {
+    const int q = p0 + e / per_pos;
+    int r = e % per_pos;
+    const int v8 = r % vec_per_col; r /= vec_per_col;
+    const int kh = r % c.kv; r /= c.kv;
+    const int kvsel = r % 2;
+    const int l = r / 2;
+    const int page = c.pt[(size_t)slot * c.max_pages + q / c.page_size];
+    const size_t off = ((((size_t)l * c.n_pages + page) * 2 + kvsel) * c.kv + kh) * (size_t)c.page_size * c.hd +
+                       (size_t)(q % c.page_size) * c.hd + (size_t)v8 * 8;
+    *reinterpret_cast<uint4*>(c.dst + off) = *reinterpret_cast<const uint4*>(c.src + off);
+  }
+}
+
+__global__ void k_copy_cols(ColCopy c, int slot, int p0, int p1) {
+  copy_cols(c, slot, p0, p1, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
+cudaError_t launch_copy_cols(const ColCopy& c, int slot, int p0, int p1, cudaStream_t st) {
+  if (p1 <= p0) return cudaSuccess;
+  const int total = (p1 - p0) * c.L * 2 * c.kv * (c.hd / 8);
+  int blocks = (total + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_copy_cols<<<blocks, 256, 0, st>>>(c, slot, p0, p1);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ commit
+__global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
+  const int b = blockIdx.x;
+  const int slot = a.slots[b];
+  const int p = a.pos[slot];
+  const bool tr = a.gate_ran && a.trig[b];
+  const int f = a.f_tok[b];
+  const int v = tr ? a.v_tok[a.rank[b]] : -1;
+  const int kind = !tr ? 0 : (v == f ? 1 : 2);
+  if (kind == 2) copy_cols(a.copy, slot, p, p + 1, threadIdx.x, blockDim.x);  // single-column repair
+  if (threadIdx.x == 0) {
+    const int out = kind == 2 ? v : f;
+    a.tokens_out[b] = out;
+    if (a.kind_out) a.kind_out[b] = (uint8_t)kind;
+    if (a.margin_out) a.margin_out[b] = a.g[b];
+    a.hist[(size_t)slot * a.hist_stride + p + 1] = out;
+    a.pos[slot] = p + 1;
+    if (tr) a.shadow_len[slot] = p + 1;
+    if (a.dbg_vtok) {
+      a.dbg_vtok[b] = v;
+      a.dbg_vg[b] = tr ? a.v_g[a.rank[b]] : 0.f;
+      a.dbg_kind[b] = (uint8_t)kind;
+      a.dbg_trig[b] = tr ? 1 : 0;
+      a.dbg_out[b] = out;
+    }
+    const bool prot = a.prot ? a.prot[b] != 0 : true;
+    unsigned long long* s = a.stats;
+    atomicAdd(&s[1], 1ull);
+    if (prot) atomicAdd(&s[2], 1ull);
+    if (tr) atomicAdd(&s[3], 1ull);
+    if (kind == 1) atomicAdd(&s[4], 1ull);
+    if (kind == 2) atomicAdd(&s[5], 1ull);
+    if (b == 0) {
+      atomicAdd(&s[0], 1ull);
+      if (a.gate_ran && a.ctrl[0] > 0) {
+        atomicAdd(&s[6], 1ull);
+        atomicAdd(&s[7], (unsigned long long)a.ctrl[1]);
+      }
+    }
+  }
+}
+
+cudaError_t launch_commit(const CommitArgs& a, cudaStream_t st) {
+  k_commit<<<a.B, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// prefill bookkeeping: hist[slot][len] = token, pos = shadow_len = len
+__global__ void k_prefill_done(int32_t* hist, int hist_stride, int32_t* pos, int32_t* shadow_len, int slot, int len,
+                               const int32_t* tok) {
+  hist[(size_t)slot * hist_stride + len] = tok[0];
+  pos[slot] = len;
+  shadow_len[slot] = len;
+}
+
+cudaError_t launch_prefill_done(int32_t* hist, int hist_stride, int32_t* pos, int32_t* shadow_len, int slot, int len,
+                                const int32_t* tok, cudaStream_t st) {
+  k_prefill_done<<<1, 1, 0, st>>>(hist, hist_stride, pos, shadow_len, slot, len, tok);
+  return cudaGetLastError();
+}
+
+}  // namespace mg

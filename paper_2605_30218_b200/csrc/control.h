@@ -1,0 +1,74 @@
+// control.h -- argument blocks of the gate / commit kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mg {
+
+struct GateArgs {
+  const float* g;          // [B] fast margins
+  const uint8_t* prot;     // [B] or nullptr (all protected)
+  float tau;
+  const int32_t* slots;    // [B]
+  int B;
+  const int32_t* pos;      // [max_slots]
+  const int32_t* shadow_len;
+  const int32_t* hist;
+  int hist_stride;
+  uint8_t* trig;           // [B]
+  int32_t* rank;           // [B] index among gated rows, -1 if not gated
+  int32_t* ctrl;           // [2 + B]: n_gated, M, rows...
+  int32_t* last;           // [B] catch-up list index of each gated row's last token
+  int32_t* cu_slot;        // catch-up list
+  int32_t* cu_pos;
+  int32_t* cu_tok;
+  int32_t* cu_nk;
+};
+cudaError_t launch_gate(const GateArgs& a, cudaStream_t st);
+
+struct ColCopy {
+  const uint16_t* src;
+  uint16_t* dst;
+  const int32_t* pt;
+  int32_t max_pages, page_size, n_pages, L, kv, hd;
+};
+cudaError_t launch_copy_cols(const ColCopy& c, int slot, int p0, int p1, cudaStream_t st);
+
+struct CommitArgs {
+  int B;
+  const int32_t* slots;
+  const uint8_t* prot;
+  int gate_ran;
+  const uint8_t* trig;
+  const int32_t* rank;
+  const int32_t* ctrl;
+  const int32_t* f_tok;
+  const float* g;
+  const int32_t* v_tok;    // [n_gated]
+  const float* v_g;
+  int32_t* pos;
+  int32_t* shadow_len;
+  int32_t* hist;
+  int hist_stride;
+  ColCopy copy;            // shadow -> fast
+  int32_t* tokens_out;
+  uint8_t* kind_out;
+  float* margin_out;
+  unsigned long long* stats;
+  // debug record of the step (nullable)
+  int32_t* dbg_vtok;
+  float* dbg_vg;
+  uint8_t* dbg_kind;
+  uint8_t* dbg_trig;
+  int32_t* dbg_out;
+};
+cudaError_t launch_commit(const CommitArgs& a, cudaStream_t st);
+
+cudaError_t launch_prepare(const int32_t* slots, int B, const int32_t* pos, const int32_t* hist, int hist_stride,
+                           int32_t* f_slot, int32_t* f_pos, int32_t* f_tok, int32_t* f_nk, cudaStream_t st);
+cudaError_t launch_prefill_done(int32_t* hist, int hist_stride, int32_t* pos, int32_t* shadow_len, int slot, int len,
+                                const int32_t* tok, cudaStream_t st);
+cudaError_t launch_gather_rows_sub(const uint16_t* src, const int32_t* rows, int sub, int n, int d, uint16_t* dst,
+                                   cudaStream_t st);
+
+}  // namespace mg

@@ -1,0 +1,899 @@
+// engine.cu -- host orchestration of the MarginGate decode step and the C ABI
+// of include/mg.h.
+//
+// mg_decode_step:
+//   1. upload the batch (slots, protected mask, new page-table entries);
+//   2. fast path, schedule sched_fast(B, ctx): embed -> L x [rmsnorm, QKV
+//      GEMM, QKV epilogue (bias, RoPE, tentative append of column p into the
+//      FAST cache), attention, O GEMM + residual, rmsnorm,
+//      gate/up GEMM + SwiGLU, down GEMM + residual] -> final norm -> LM head
+//      -> top-2 margin;
+//   3. gate + compaction + catch-up list; the host reads
+//      the trigger count (the verifier's size is data dependent);
+//   4. verifier on the gated rows, schedule sched_det (pinned split-K per
+//      weight shape, 16-column MMA slot groups, fixed 256-key attention
+//      chunks): the catch-up tokens shadow_len..p run through the same
+//      kernels against the SHADOW cache (A1), in chunks of Tv
+//      tokens; the LM head + argmax runs on each gated row's last token;
+//   5. commit: fast / verified / single-column repair
+//      and r_verify / r_repair counters.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/mg_debug.h"
+#include "engine.h"
+
+using namespace mg;
+
+namespace {
+
+constexpr int kSMs = 148;
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base((char*)b) {}
+  template <class T>
+  T* take(size_t n) {
+    T* p = (T*)(base ? base + off : nullptr);
+    off += align256(n * sizeof(T));
+    return p;
+  }
+};
+
+bool valid_cfg(const mg_config* c, std::string* why) {
+  auto bad = [&](const char* m) {
+    if (why) *why = m;
+    return false;
+  };
+  if (!c) return bad("null config");
+  if (c->n_layers < 1 || c->d_model < 64 || c->n_heads < 1 || c->n_kv_heads < 1) return bad("bad shape");
+  if (c->head_dim != 64 && c->head_dim != 128) return bad("head_dim must be 64 or 128");
+  if (c->n_heads % c->n_kv_heads) return bad("n_heads % n_kv_heads != 0");
+  if (c->n_heads / c->n_kv_heads > 8) return bad("GQA group > 8 unsupported");
+  if (c->d_model % 64 || c->d_ff % 64) return bad("d_model and d_ff must be multiples of 64");
+  if (((c->n_heads + 2 * c->n_kv_heads) * c->head_dim) % 128) return bad("(H+2KV)*hd must be a multiple of 128");
+  if ((c->n_heads * c->head_dim) % 64) return bad("H*hd must be a multiple of 64");
+  if (c->d_model % 128) return bad("d_model must be a multiple of 128");
+  if (c->vocab % 128) return bad("vocab must be a multiple of 128");
+  if (c->max_batch < 1 || c->max_batch > 256) return bad("max_batch must be in [1, 256]");
+  if (c->max_slots < c->max_batch) return bad("max_slots < max_batch");
+  if (c->max_seq < 2) return bad("max_seq < 2");
+  if (c->page_size != 16 && c->page_size != 32 && c->page_size != 64) return bad("page_size must be 16, 32 or 64");
+  if (c->verify_chunk < 0 || c->verify_chunk > 1024) return bad("verify_chunk must be in [0, 1024]");
+  if (!(c->rms_eps >= 0.f) || !(c->rope_theta > 0.f)) return bad("bad eps/theta");
+  return true;
+}
+
+int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
+int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// ---- schedules (A13/A14) -------------------------------------
+int splits_for(int N, int K, int T, int tile_n, int impl) {
+  const int KB = K / 64;
+  const int tiles = impl == 0 ? (N / 128) * cdiv(T, tile_n) : cdiv(N, 8);
+  const int S = cdiv(2 * kSMs, tiles);
+  int smax = KB / 4;
+  if (smax < 1) smax = 1;
+  return clampi(S, 1, smax < 16 ? smax : 16);
+}
+
+OpSched op_fast(int N, int K, int T) {
+  OpSched o;
+  o.impl = T <= 4 ? 1 : 0;
+  o.tile_n = gemm_tile_n(T);
+  o.mma_n = o.tile_n;
+  o.splits = splits_for(N, K, T, o.tile_n, o.impl);
+  return o;
+}
+OpSched op_det(int N, int K, int T) {
+  OpSched o;
+  o.impl = 0;
+  o.tile_n = gemm_tile_n(T);
+  o.mma_n = 16;                                // pinned 16-column slot groups
+  o.splits = splits_for(N, K, 16, 16, 0);      // depends on the weight shape only
+  return o;
+}
+
+}  // namespace
+
+static Sched sched_fast(const mg_ctx* c, int T, int max_ctx) {
+  Sched s;
+  s.qkv = op_fast(c->NQKV, c->d, T);
+  s.o = op_fast(c->d, c->NQ, T);
+  s.gu = op_fast(2 * c->F, c->d, T);
+  s.down = op_fast(c->d, c->F, T);
+  s.lm = op_fast(c->V, c->d, T);
+  s.lm.splits = 1;
+  int nch = clampi(cdiv(2 * kSMs, T * c->KV), 1, 32);
+  int chunk = cdiv(cdiv(max_ctx, nch), 16) * 16;
+  chunk = clampi(chunk, 16, 512);
+  s.attn_chunk = chunk;
+  s.attn_nch = cdiv(max_ctx, chunk);
+  return s;
+}
+
+static Sched sched_det(const mg_ctx* c, int T, int max_ctx) {
+  Sched s;
+  s.qkv = op_det(c->NQKV, c->d, T);
+  s.o = op_det(c->d, c->NQ, T);
+  s.gu = op_det(2 * c->F, c->d, T);
+  s.down = op_det(c->d, c->F, T);
+  s.lm = op_det(c->V, c->d, T);
+  s.lm.splits = 1;
+  s.attn_chunk = 256;
+  s.attn_nch = cdiv(max_ctx, 256);
+  return s;
+}
+
+// ------------------------------------------------------------------ errors
+static mg_status fail(mg_ctx* c, mg_status s, const std::string& m) {
+  c->err = m;
+  if (s == MG_ERR_CUDA) c->dead = true;
+  return s;
+}
+#define CK(expr)                                                                                  \
+  do {                                                                                            \
+    cudaError_t _e = (expr);                                                                      \
+    if (_e != cudaSuccess) return fail(c, MG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+// ------------------------------------------------------------------ layout
+struct Layout {
+  size_t weights, kv, workspace;
+};
+
+static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout* lay) {
+  const mg_config& g = c->cfg;
+  c->L = g.n_layers; c->d = g.d_model; c->H = g.n_heads; c->KV = g.n_kv_heads; c->hd = g.head_dim;
+  c->F = g.d_ff; c->V = g.vocab;
+  c->NQ = c->H * c->hd; c->NK = c->KV * c->hd; c->NQKV = c->NQ + 2 * c->NK;
+  c->Tv = g.verify_chunk > 0 ? g.verify_chunk : 512;
+  c->Tmax = g.max_batch > c->Tv ? g.max_batch : c->Tv;
+  c->PS = g.page_size;
+  c->max_pages = cdiv(g.max_seq, c->PS);
+  c->n_pages = g.max_slots * c->max_pages;
+  c->nb_top2 = top2_blocks(c->V);
+
+  Carver w(wbase);
+  c->embed = w.take<uint16_t>((size_t)c->V * c->d);
+  c->layers.resize(c->L);
+  for (auto& l : c->layers) {
+    l.attn_norm = w.take<uint16_t>(c->d);
+    l.qkv.ptr = w.take<uint16_t>((size_t)c->NQKV * c->d); l.qkv.N = c->NQKV; l.qkv.K = c->d;
+    l.bqkv = g.qkv_bias ? w.take<uint16_t>(c->NQKV) : nullptr;
+    l.o.ptr = w.take<uint16_t>((size_t)c->d * c->NQ); l.o.N = c->d; l.o.K = c->NQ;
+    l.mlp_norm = w.take<uint16_t>(c->d);
+    l.gu.ptr = w.take<uint16_t>((size_t)2 * c->F * c->d); l.gu.N = 2 * c->F; l.gu.K = c->d;
+    l.down.ptr = w.take<uint16_t>((size_t)c->d * c->F); l.down.N = c->d; l.down.K = c->F;
+  }
+  c->final_norm = w.take<uint16_t>(c->d);
+  c->lm.ptr = w.take<uint16_t>((size_t)c->V * c->d); c->lm.N = c->V; c->lm.K = c->d;
+  lay->weights = w.off;
+
+  lay->kv = align256((size_t)c->L * c->n_pages * 2 * c->KV * c->PS * c->hd * sizeof(uint16_t));
+  c->kv_fast = (uint16_t*)kvf;
+  c->kv_shadow = (uint16_t*)kvs;
+
+  // GEMM partial buffer: max over ops of S x T x N for the fast (T <= max_batch)
+  // and det (T <= Tv) schedules
+  size_t pe = (size_t)g.max_batch * c->V;  // LM logits share the buffer only if larger
+  auto upd = [&](const Sched& s, int T) {
+    const size_t v[4] = {(size_t)s.qkv.splits * T * c->NQKV, (size_t)s.o.splits * T * c->d,
+                         (size_t)s.gu.splits * T * 2 * c->F, (size_t)s.down.splits * T * c->d};
+    for (size_t x : v) pe = x > pe ? x : pe;
+  };
+  for (int T = 1; T <= g.max_batch; ++T) upd(sched_fast(c, T, g.max_seq), T);
+  for (int T = 1; T <= c->Tv; T = T < 16 ? T + 1 : T + 16) upd(sched_det(c, T, g.max_seq), T);
+  upd(sched_det(c, c->Tv, g.max_seq), c->Tv);
+  c->part_elems = pe;
+  c->nch_max = cdiv(g.max_seq, 16);
+  if (c->nch_max > 512) c->nch_max = 512;
+  size_t attn_rows_fast = (size_t)g.max_batch * c->H * 33;
+  size_t attn_rows_det = (size_t)c->Tv * c->H * cdiv(g.max_seq, 256);
+  size_t attn_rows = attn_rows_fast > attn_rows_det ? attn_rows_fast : attn_rows_det;
+
+  Carver s(ws);
+  const int Tm = c->Tmax, B = g.max_batch;
+  c->x = s.take<uint16_t>((size_t)Tm * c->d);
+  c->xn = s.take<uint16_t>((size_t)Tm * c->d);
+  c->q = s.take<uint16_t>((size_t)Tm * c->NQ);
+  c->att = s.take<uint16_t>((size_t)Tm * c->NQ);
+  c->a = s.take<uint16_t>((size_t)Tm * c->F);
+  c->xg = s.take<uint16_t>((size_t)B * c->d);
+  c->xgn = s.take<uint16_t>((size_t)B * c->d);
+  c->part = s.take<float>(c->part_elems);
+  c->logits = s.take<float>((size_t)B * c->V);
+  c->attn_acc = s.take<float>(attn_rows * c->hd);
+  c->attn_ml = s.take<float>(attn_rows * 2);
+  c->top2_part = s.take<float>((size_t)Tm * c->nb_top2 * 4);
+  c->rope_cos = s.take<float>((size_t)g.max_seq * (c->hd / 2));
+  c->rope_sin = s.take<float>((size_t)g.max_seq * (c->hd / 2));
+  c->pos_d = s.take<int32_t>(g.max_slots);
+  c->shadow_d = s.take<int32_t>(g.max_slots);
+  c->hist_d = s.take<int32_t>((size_t)g.max_slots * (g.max_seq + 1));
+  c->pt_d = s.take<int32_t>((size_t)g.max_slots * c->max_pages);
+  c->stats_d = s.take<unsigned long long>(16);
+  c->nan_d = s.take<int32_t>(4);
+  c->slots_d = s.take<int32_t>(B);
+  c->prot_d = s.take<uint8_t>(B);
+  c->f_slot = s.take<int32_t>(B); c->f_pos = s.take<int32_t>(B); c->f_tok = s.take<int32_t>(B);
+  c->f_nk = s.take<int32_t>(B); c->f_i2 = s.take<int32_t>(B);
+  c->f_g = s.take<float>(B); c->f_v1 = s.take<float>(B); c->f_v2 = s.take<float>(B);
+  c->trig_d = s.take<uint8_t>(B);
+  c->rank_d = s.take<int32_t>(B);
+  c->ctrl_d = s.take<int32_t>(2 + B);
+  c->last_d = s.take<int32_t>(B);
+  const size_t cu = (size_t)B * g.max_seq > (size_t)Tm ? (size_t)B * g.max_seq : (size_t)Tm;
+  c->cu_slot = s.take<int32_t>(cu); c->cu_pos = s.take<int32_t>(cu);
+  c->cu_tok = s.take<int32_t>(cu); c->cu_nk = s.take<int32_t>(cu);
+  c->v_tok = s.take<int32_t>(B); c->v_i2 = s.take<int32_t>(B);
+  c->v_g = s.take<float>(B); c->v_v1 = s.take<float>(B); c->v_v2 = s.take<float>(B);
+  {
+    const size_t a4 = 4 * (size_t)B, b2 = 2 * (size_t)c->max_pages;
+    c->staging_d = s.take<int32_t>((a4 > b2 ? a4 : b2) + 64);
+  }
+  c->dbg_vtok = s.take<int32_t>(B); c->dbg_out = s.take<int32_t>(B);
+  c->dbg_vg = s.take<float>(B);
+  c->dbg_kind = s.take<uint8_t>(B); c->dbg_trig = s.take<uint8_t>(B);
+  lay->workspace = s.off;
+}
+
+// ------------------------------------------------------------------ launch helpers
+static CacheView cache_view(const mg_ctx* c, int which, int layer) {
+  CacheView v;
+  v.pool = which ? c->kv_shadow : c->kv_fast;
+  v.pt = c->pt_d;
+  v.max_pages = c->max_pages;
+  v.page_size = c->PS;
+  v.n_pages = c->n_pages;
+  v.layer = layer;
+  v.kv = c->KV;
+  v.hd = c->hd;
+  return v;
+}
+
+static ColCopy col_copy(const mg_ctx* c, bool shadow_to_fast) {
+  ColCopy cc;
+  cc.src = shadow_to_fast ? c->kv_shadow : c->kv_fast;
+  cc.dst = shadow_to_fast ? c->kv_fast : c->kv_shadow;
+  cc.pt = c->pt_d;
+  cc.max_pages = c->max_pages;
+  cc.page_size = c->PS;
+  cc.n_pages = c->n_pages;
+  cc.L = c->L;
+  cc.kv = c->KV;
+  cc.hd = c->hd;
+  return cc;
+}
+
+static const CUtensorMap* xmap(mg_ctx* c, const void* buf, int K, int rows, int box) {
+  auto key = std::make_tuple(buf, K, rows, box);
+  auto it = c->xmaps.find(key);
+  if (it != c->xmaps.end()) return &it->second;
+  CUtensorMap m;
+  if (!make_tmap_2d(&m, buf, K, rows, box)) return nullptr;
+  return &(c->xmaps[key] = m);
+}
+
+static cudaEvent_t tevent(mg_ctx* c) {
+  auto& t = c->timing;
+  if (t.used == t.pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    t.pool.push_back(e);
+  }
+  return t.pool[t.used++];
+}
+
+static mg_status gemm(mg_ctx* c, const uint16_t* X, int xrows, int T, const Weight& W, const OpSched& o, float* out) {
+  size_t i0 = 0;
+  if (c->timing.on) {
+    i0 = c->timing.used;
+    cudaEventRecord(tevent(c), c->st);
+  }
+  if (o.impl == 1) {
+    CK(launch_gemm_cc(X, W.ptr, W.N, W.K, T, o.splits, out, c->st));
+  } else {
+    const CUtensorMap* mx = xmap(c, X, W.K, xrows, o.tile_n);
+    if (!mx) return fail(c, MG_ERR_CUDA, "cuTensorMapEncodeTiled failed for activations");
+    CK(launch_gemm_tc(W.map, *mx, W.N, W.K, T, o.splits, o.tile_n, o.mma_n, out, c->st));
+  }
+  c->launches += 1;
+  if (c->timing.on) {
+    cudaEventRecord(tevent(c), c->st);
+    const double bytes = (double)W.N * W.K * 2 + (double)T * W.K * 2 + (double)o.splits * T * W.N * 4;
+    c->timing.rec.emplace_back(i0, i0 + 1, 0, bytes);
+  }
+  return MG_OK;
+}
+
+// One forward over T tokens (token list slot/pos/tok/nk on device), against
+// cache `which` (0 fast, 1 shadow), leaving the residual stream in c->x.
+static mg_status forward(mg_ctx* c, int T, const int32_t* slot, const int32_t* pos, const int32_t* tok,
+                         const int32_t* nk, int which, const Sched& sc) {
+  const int Tm = c->Tmax;
+  CK(launch_embed(c->embed, tok, T, c->d, c->x, c->st));
+  c->launches++;
+  for (int l = 0; l < c->L; ++l) {
+    const LayerW& w = c->layers[l];
+    CK(launch_rmsnorm(c->x, w.attn_norm, T, c->d, c->cfg.rms_eps, c->xn, c->st));
+    mg_status r = gemm(c, c->xn, Tm, T, w.qkv, sc.qkv, c->part);
+    if (r) return r;
+    CacheView cv = cache_view(c, which, l);
+    CK(launch_epi_qkv(c->part, sc.qkv.splits, w.bqkv, pos, T, c->H, c->KV, c->hd, c->rope_cos, c->rope_sin, c->q,
+                      &cv, slot, nullptr, nullptr, c->st));
+    AttnArgs aa{};
+    aa.q = c->q; aa.cache = cv; aa.paged = 1; aa.slot = slot; aa.n_keys = nk;
+    aa.T = T; aa.H = c->H; aa.KV = c->KV; aa.hd = c->hd; aa.chunk = sc.attn_chunk; aa.n_chunks = sc.attn_nch;
+    aa.part_acc = c->attn_acc; aa.part_ml = c->attn_ml; aa.out = c->att;
+    size_t i0 = 0;
+    if (c->timing.on) { i0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
+    CK(launch_attention(aa, c->st));
+    if (c->timing.on) {
+      cudaEventRecord(tevent(c), c->st);
+      c->timing.rec.emplace_back(i0, i0 + 1, 1, 0.0);
+    }
+    if ((r = gemm(c, c->att, Tm, T, w.o, sc.o, c->part))) return r;
+    CK(launch_epi_residual(c->x, c->part, sc.o.splits, T, c->d, c->x, c->st));
+    CK(launch_rmsnorm(c->x, w.mlp_norm, T, c->d, c->cfg.rms_eps, c->xn, c->st));
+    if ((r = gemm(c, c->xn, Tm, T, w.gu, sc.gu, c->part))) return r;
+    CK(launch_epi_swiglu(c->part, sc.gu.splits, T, c->F, c->a, c->st));
+    if ((r = gemm(c, c->a, Tm, T, w.down, sc.down, c->part))) return r;
+    CK(launch_epi_residual(c->x, c->part, sc.down.splits, T, c->d, c->x, c->st));
+    c->launches += 8;
+  }
+  return MG_OK;
+}
+
+// final norm + LM head + top-2 over rows xin[0..T)
+static mg_status lm_head(mg_ctx* c, const uint16_t* xin, uint16_t* xnorm, int xrows, int T, const OpSched& o,
+                         float* v1, int32_t* i1, float* v2, int32_t* i2, float* g) {
+  CK(launch_rmsnorm(xin, c->final_norm, T, c->d, c->cfg.rms_eps, xnorm, c->st));
+  mg_status r = gemm(c, xnorm, xrows, T, c->lm, o, c->logits);
+  if (r) return r;
+  CK(launch_top2(c->logits, T, c->V, c->top2_part, c->nb_top2, v1, i1, v2, i2, g, c->nan_d, c->st));
+  c->launches += 3;
+  return MG_OK;
+}
+
+static mg_status alloc_page(mg_ctx* c, int slot, std::vector<std::pair<int, int>>* upd) {
+  if (c->free_pages.empty()) return fail(c, MG_ERR_CAPACITY, "KV pages exhausted");
+  const int p = c->free_pages.back();
+  c->free_pages.pop_back();
+  const int idx = (int)c->pages[slot].size();
+  c->pages[slot].push_back(p);
+  upd->emplace_back(slot * c->max_pages + idx, p);
+  return MG_OK;
+}
+
+__global__ void k_apply_pt(int32_t* pt, const int32_t* upd, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) pt[upd[2 * i]] = upd[2 * i + 1];
+}
+
+// stage `words` int32 into pinned memory and copy them to staging_d
+static mg_status upload(mg_ctx* c, const std::vector<int32_t>& words) {
+  // pinned layout: [stage0 | stage1 | ctrl (2 + max_batch)]
+  if (words.size() > c->stage_words) return fail(c, MG_ERR_INVALID, "staging overflow");
+  const int i = c->stage_idx;
+  c->stage_idx ^= 1;
+  CK(cudaEventSynchronize(c->stage_ev[i]));
+  int32_t* h = c->pinned + i * c->stage_words;
+  memcpy(h, words.data(), words.size() * 4);
+  CK(cudaMemcpyAsync(c->staging_d, h, words.size() * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaEventRecord(c->stage_ev[i], c->st));
+  return MG_OK;
+}
+
+static mg_status apply_pt(mg_ctx* c, const std::vector<std::pair<int, int>>& upd) {
+  if (upd.empty()) return MG_OK;
+  std::vector<int32_t> w;
+  for (auto& u : upd) { w.push_back(u.first); w.push_back(u.second); }
+  mg_status r = upload(c, w);
+  if (r) return r;
+  k_apply_pt<<<cdiv((int)upd.size(), 128), 128, 0, c->st>>>(c->pt_d, c->staging_d, (int)upd.size());
+  CK(cudaGetLastError());
+  c->launches++;
+  return MG_OK;
+}
+
+// Runs the deterministic schedule over a token list already on device
+// (cu_* arrays, entries [0, M)), in chunks of Tv tokens, then the LM head +
+// top-2 on the rows' last tokens `last_host` (list indices, ascending),
+// writing v arrays [0, n_last).
+static mg_status run_det(mg_ctx* c, int M, const std::vector<int>& last_host, int max_ctx_hint) {
+  int r0 = 0;  // next gated row whose last token is pending
+  const int n_last = (int)last_host.size();
+  for (int c0 = 0; c0 < M; c0 += c->Tv) {
+    const int T = M - c0 < c->Tv ? M - c0 : c->Tv;
+    Sched sc = sched_det(c, T, max_ctx_hint);
+    mg_status r = forward(c, T, c->cu_slot + c0, c->cu_pos + c0, c->cu_tok + c0, c->cu_nk + c0, 1, sc);
+    if (r) return r;
+    int r1 = r0;
+    while (r1 < n_last && last_host[r1] < c0 + T) ++r1;
+    if (r1 > r0) {
+      CK(launch_gather_rows_sub(c->x, c->last_d + r0, c0, r1 - r0, c->d, c->xg, c->st));
+      c->launches++;
+      if ((r = lm_head(c, c->xg, c->xgn, c->cfg.max_batch, r1 - r0, sc.lm, c->v_v1 + r0, c->v_tok + r0,
+                       c->v_v2 + r0, c->v_i2 + r0, c->v_g + r0)))
+        return r;
+    }
+    r0 = r1;
+  }
+  return MG_OK;
+}
+
+static size_t stage_words(const mg_ctx* c) {
+  const size_t a = 4 * (size_t)c->cfg.max_batch, b = 2 * (size_t)c->max_pages;
+  return (a > b ? a : b) + 64;
+}
+
+static void init_rope(const mg_config& g, std::vector<float>& cs, std::vector<float>& sn) {
+  const int h2 = g.head_dim / 2;
+  cs.resize((size_t)g.max_seq * h2);
+  sn.resize((size_t)g.max_seq * h2);
+  for (int p = 0; p < g.max_seq; ++p)
+    for (int i = 0; i < h2; ++i) {
+      const double inv = pow((double)g.rope_theta, -(2.0 * (double)i) / (double)g.head_dim);
+      const double ang = (double)p * inv;
+      cs[(size_t)p * h2 + i] = (float)cos(ang);
+      sn[(size_t)p * h2 + i] = (float)sin(ang);
+    }
+}
+
+static mg_status gen_weights(mg_ctx* c) {
+  const uint64_t seed = c->cfg.weight_seed;
+  const int L = c->L;
+  auto tid = [&](int layer, int which) -> uint32_t {
+    if (layer < 0) return which == 0 ? 0u : (uint32_t)(1 + 16 * L + (which - 1));
+    return (uint32_t)(1 + 16 * layer + which);
+  };
+  auto gen = [&](uint32_t t, int64_t n, int kind, int fan, uint16_t* dst, int remap = 0, int row_len = 0) {
+    GenSpec g{seed, t, n, kind, fan, row_len, remap};
+    c->launches++;
+    return launch_gen(g, dst, c->st);
+  };
+  CK(gen(tid(-1, 0), (int64_t)c->V * c->d, 1, 0, c->embed));
+  CK(gen(tid(-1, 1), c->d, 2, 0, c->final_norm));
+  CK(gen(tid(-1, 2), (int64_t)c->V * c->d, 0, c->d, c->lm.ptr));
+  for (int l = 0; l < L; ++l) {
+    LayerW& w = c->layers[l];
+    CK(gen(tid(l, 0), c->d, 2, 0, w.attn_norm));
+    CK(gen(tid(l, 1), (int64_t)c->NQ * c->d, 0, c->d, w.qkv.ptr));
+    CK(gen(tid(l, 2), (int64_t)c->NK * c->d, 0, c->d, w.qkv.ptr + (size_t)c->NQ * c->d));
+    CK(gen(tid(l, 3), (int64_t)c->NK * c->d, 0, c->d, w.qkv.ptr + (size_t)(c->NQ + c->NK) * c->d));
+    CK(gen(tid(l, 4), (int64_t)c->d * c->NQ, 0, c->NQ, w.o.ptr));
+    CK(gen(tid(l, 5), c->d, 2, 0, w.mlp_norm));
+    CK(gen(tid(l, 6), (int64_t)c->F * c->d, 0, c->d, w.gu.ptr, 1, c->d));
+    CK(gen(tid(l, 7), (int64_t)c->F * c->d, 0, c->d, w.gu.ptr, 2, c->d));
+    CK(gen(tid(l, 8), (int64_t)c->d * c->F, 0, c->F, w.down.ptr));
+    if (w.bqkv) {
+      CK(gen(tid(l, 9), c->NQ, 3, 0, w.bqkv));
+      CK(gen(tid(l, 10), c->NK, 3, 0, w.bqkv + c->NQ));
+      CK(gen(tid(l, 11), c->NK, 3, 0, w.bqkv + c->NQ + c->NK));
+    }
+  }
+  return MG_OK;
+}
+
+// ================================================================== C ABI
+static std::string g_init_err;
+
+extern "C" {
+
+mg_status mg_query_sizes(const mg_config* cfg, mg_sizes* out) {
+  std::string why;
+  if (!out || !valid_cfg(cfg, &why)) {
+    g_init_err = why.empty() ? "null output" : why;
+    return MG_ERR_INVALID;
+  }
+  mg_ctx tmp;
+  tmp.cfg = *cfg;
+  Layout lay;
+  carve(&tmp, nullptr, nullptr, nullptr, nullptr, &lay);
+  out->weights = lay.weights;
+  out->kv_fast = lay.kv;
+  out->kv_shadow = lay.kv;
+  out->workspace = lay.workspace;
+  return MG_OK;
+}
+
+mg_status mg_init(const mg_config* cfg, const mg_buffers* bufs, void* stream, mg_ctx** out) {
+  std::string why;
+  if (!out || !bufs || !valid_cfg(cfg, &why)) {
+    g_init_err = why.empty() ? "null argument" : why;
+    return MG_ERR_INVALID;
+  }
+  *out = nullptr;
+  if (!bufs->weights || !bufs->kv_fast || !bufs->kv_shadow || !bufs->workspace) {
+    g_init_err = "null buffer";
+    return MG_ERR_INVALID;
+  }
+  mg_ctx* c = new mg_ctx();
+  c->cfg = *cfg;
+  c->buf = *bufs;
+  c->st = (cudaStream_t)stream;
+  cudaGetDevice(&c->dev);
+  Layout lay;
+  carve(c, bufs->weights, bufs->kv_fast, bufs->kv_shadow, bufs->workspace, &lay);
+  auto die = [&](const std::string& m) {
+    g_init_err = m;
+    delete c;
+    return MG_ERR_CUDA;
+  };
+  // tensor maps of the weights (box: 64 k x 128 rows)
+  for (auto& l : c->layers)
+    for (Weight* w : {&l.qkv, &l.o, &l.gu, &l.down})
+      if (!make_tmap_2d(&w->map, w->ptr, w->K, w->N, 128)) return die("cuTensorMapEncodeTiled failed (weights)");
+  if (!make_tmap_2d(&c->lm.map, c->lm.ptr, c->lm.K, c->lm.N, 128)) return die("cuTensorMapEncodeTiled failed (lm)");
+
+  std::vector<float> cs, sn;
+  init_rope(c->cfg, cs, sn);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(bufs->workspace, 0, lay.workspace, c->st)) ||
+      (e = cudaMemcpyAsync(c->rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, c->st)) ||
+      (e = cudaMemcpyAsync(c->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice, c->st)))
+    return die(cudaGetErrorString(e));
+  if (gen_weights(c) != MG_OK) return die(c->err);
+  if ((e = cudaStreamSynchronize(c->st))) return die(cudaGetErrorString(e));
+  c->stage_words = stage_words(c);
+  c->pinned_words = 2 * c->stage_words + 2 + c->cfg.max_batch;
+  if ((e = cudaMallocHost(&c->pinned, c->pinned_words * 4)) || (e = cudaEventCreate(&c->stage_ev[0])) ||
+      (e = cudaEventCreate(&c->stage_ev[1])))
+    return die(cudaGetErrorString(e));
+  cudaEventRecord(c->stage_ev[0], c->st);
+  cudaEventRecord(c->stage_ev[1], c->st);
+  c->pos_h.assign(c->cfg.max_slots, 0);
+  c->shadow_h.assign(c->cfg.max_slots, 0);
+  c->active.assign(c->cfg.max_slots, 0);
+  c->pages.assign(c->cfg.max_slots, {});
+  for (int p = c->n_pages - 1; p >= 0; --p) c->free_pages.push_back(p);
+  *out = c;
+  return MG_OK;
+}
+
+mg_status mg_prefill(mg_ctx* c, int32_t slot, const int32_t* prompt, int32_t len, int32_t* first_token) {
+  if (!c) return MG_ERR_INVALID;
+  if (c->dead) return fail(c, MG_ERR_CUDA, "context is dead: " + c->err);
+  if (slot < 0 || slot >= c->cfg.max_slots || !prompt || len < 1 || !first_token)
+    return fail(c, MG_ERR_INVALID, "bad prefill arguments");
+  if (c->active[slot]) return fail(c, MG_ERR_STATE, "slot already active");
+  if (len + 1 > c->cfg.max_seq) return fail(c, MG_ERR_CAPACITY, "prompt longer than max_seq - 1");
+  for (int i = 0; i < len; ++i)
+    if (prompt[i] < 0 || prompt[i] >= c->V) return fail(c, MG_ERR_INVALID, "token id out of range");
+  const int need = cdiv(len, c->PS);
+  if ((int)c->free_pages.size() < need) return fail(c, MG_ERR_CAPACITY, "KV pages exhausted");
+  std::vector<std::pair<int, int>> upd;
+  for (int i = 0; i < need; ++i) alloc_page(c, slot, &upd);
+  mg_status r = apply_pt(c, upd);
+  if (r) return r;
+  // token list: (slot, q, prompt[q], q+1); history row
+  std::vector<int32_t> sl(len, slot), ps(len), nk(len);
+  for (int i = 0; i < len; ++i) { ps[i] = i; nk[i] = i + 1; }
+  CK(cudaMemcpyAsync(c->cu_slot, sl.data(), len * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->cu_pos, ps.data(), len * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->cu_tok, prompt, len * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->cu_nk, nk.data(), len * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->hist_d + (size_t)slot * (c->cfg.max_seq + 1), prompt, len * 4, cudaMemcpyHostToDevice,
+                     c->st));
+  int32_t last = len - 1;
+  CK(cudaMemcpyAsync(c->last_d, &last, 4, cudaMemcpyHostToDevice, c->st));
+  if ((r = run_det(c, len, std::vector<int>{len - 1}, len))) return r;
+  CK(launch_copy_cols(col_copy(c, true), slot, 0, len, c->st));
+  CK(launch_prefill_done(c->hist_d, c->cfg.max_seq + 1, c->pos_d, c->shadow_d, slot, len, c->v_tok, c->st));
+  c->launches += 2;
+  CK(cudaMemcpyAsync(first_token, c->v_tok, 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->pos_h[slot] = len;
+  c->shadow_h[slot] = len;
+  c->active[slot] = 1;
+  return MG_OK;
+}
+
+mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8_t* prot, float tau,
+                         int32_t* tokens_out, uint8_t* kind_out, float* margin_out) {
+  if (!c) return MG_ERR_INVALID;
+  if (c->dead) return fail(c, MG_ERR_CUDA, "context is dead: " + c->err);
+  if (!slots || !tokens_out || B < 1 || B > c->cfg.max_batch) return fail(c, MG_ERR_INVALID, "bad batch");
+  if (std::isnan(tau) || tau < 0.f) return fail(c, MG_ERR_INVALID, "threshold must be >= 0");
+  std::vector<char> seen(c->cfg.max_slots, 0);
+  int max_ctx = 1;
+  int need_pages = 0;
+  bool any_prot = false;
+  for (int b = 0; b < B; ++b) {
+    const int s = slots[b];
+    if (s < 0 || s >= c->cfg.max_slots || !c->active[s] || seen[s])
+      return fail(c, MG_ERR_INVALID, "inactive or duplicate slot");
+    seen[s] = 1;
+    const int p = c->pos_h[s];
+    if (p >= c->cfg.max_seq) return fail(c, MG_ERR_CAPACITY, "max_seq reached");
+    if (p / c->PS >= (int)c->pages[s].size()) ++need_pages;
+    if (p + 1 > max_ctx) max_ctx = p + 1;
+    if (!prot || prot[b]) any_prot = true;
+  }
+  if ((int)c->free_pages.size() < need_pages) return fail(c, MG_ERR_CAPACITY, "KV pages exhausted");
+  size_t ev0 = 0;
+  if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
+
+  // 1. upload batch + page-table updates (one H2D copy)
+  std::vector<std::pair<int, int>> upd;
+  for (int b = 0; b < B; ++b) {
+    const int s = slots[b];
+    if (c->pos_h[s] / c->PS >= (int)c->pages[s].size()) alloc_page(c, s, &upd);
+  }
+  {
+    const int pw = (B + 3) / 4;  // prot bytes packed in words
+    std::vector<int32_t> w(B + pw + 2 * upd.size());
+    memcpy(w.data(), slots, B * 4);
+    std::vector<uint8_t> pb(pw * 4, 1);
+    if (prot) memcpy(pb.data(), prot, B);
+    memcpy(w.data() + B, pb.data(), pw * 4);
+    for (size_t i = 0; i < upd.size(); ++i) {
+      w[B + pw + 2 * i] = upd[i].first;
+      w[B + pw + 2 * i + 1] = upd[i].second;
+    }
+    mg_status r = upload(c, w);
+    if (r) return r;
+    CK(cudaMemcpyAsync(c->slots_d, c->staging_d, B * 4, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(c->prot_d, c->staging_d + B, B, cudaMemcpyDeviceToDevice, c->st));
+    if (!upd.empty()) {
+      k_apply_pt<<<cdiv((int)upd.size(), 128), 128, 0, c->st>>>(c->pt_d, c->staging_d + B + pw, (int)upd.size());
+      CK(cudaGetLastError());
+      c->launches++;
+    }
+  }
+  // 2. fast path
+  CK(launch_prepare(c->slots_d, B, c->pos_d, c->hist_d, c->cfg.max_seq + 1, c->f_slot, c->f_pos, c->f_tok, c->f_nk,
+                    c->st));
+  c->launches++;
+  Sched fs = sched_fast(c, B, max_ctx);
+  mg_status r = forward(c, B, c->f_slot, c->f_pos, c->f_tok, c->f_nk, 0, fs);
+  if (r) return r;
+  if ((r = lm_head(c, c->x, c->xn, c->Tmax, B, fs.lm, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g))) return r;
+  if (c->capture) CK(cudaMemcpyAsync(c->capture, c->logits, (size_t)B * c->V * 4, cudaMemcpyDeviceToDevice, c->st));
+
+  // 3. gate (+ 4. verifier)
+  const bool gate = any_prot && tau > 0.f;
+  int n_gated = 0;
+  std::vector<int> rows;
+  if (gate) {
+    GateArgs ga{};
+    ga.g = c->f_g; ga.prot = c->prot_d; ga.tau = tau; ga.slots = c->slots_d; ga.B = B;
+    ga.pos = c->pos_d; ga.shadow_len = c->shadow_d; ga.hist = c->hist_d; ga.hist_stride = c->cfg.max_seq + 1;
+    ga.trig = c->trig_d; ga.rank = c->rank_d; ga.ctrl = c->ctrl_d; ga.last = c->last_d;
+    ga.cu_slot = c->cu_slot; ga.cu_pos = c->cu_pos; ga.cu_tok = c->cu_tok; ga.cu_nk = c->cu_nk;
+    CK(launch_gate(ga, c->st));
+    c->launches++;
+    int32_t* ctrl_h = c->pinned + (c->pinned_words - (2 + c->cfg.max_batch));
+    CK(cudaMemcpyAsync(ctrl_h, c->ctrl_d, (2 + B) * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    n_gated = ctrl_h[0];
+    const int M = ctrl_h[1];
+    rows.assign(ctrl_h + 2, ctrl_h + 2 + n_gated);
+    if (n_gated > 0) {
+      std::vector<int> last;
+      int off = 0, vmax = 1;
+      for (int i = 0; i < n_gated; ++i) {
+        const int s = slots[rows[i]];
+        const int gap = c->pos_h[s] - c->shadow_h[s] + 1;
+        off += gap;
+        last.push_back(off - 1);
+        if (c->pos_h[s] + 1 > vmax) vmax = c->pos_h[s] + 1;
+      }
+      if (off != M) return fail(c, MG_ERR_CUDA, "catch-up size mismatch between host mirror and device");
+      if ((r = run_det(c, M, last, vmax))) return r;
+    }
+  }
+  // 5. commit
+  CommitArgs ca{};
+  ca.B = B; ca.slots = c->slots_d; ca.prot = c->prot_d; ca.gate_ran = gate ? 1 : 0; ca.trig = c->trig_d;
+  ca.rank = c->rank_d; ca.ctrl = c->ctrl_d; ca.f_tok = c->f_tok; ca.g = c->f_g; ca.v_tok = c->v_tok; ca.v_g = c->v_g;
+  ca.pos = c->pos_d; ca.shadow_len = c->shadow_d; ca.hist = c->hist_d; ca.hist_stride = c->cfg.max_seq + 1;
+  ca.copy = col_copy(c, true);
+  ca.tokens_out = tokens_out; ca.kind_out = kind_out; ca.margin_out = margin_out; ca.stats = c->stats_d;
+  ca.dbg_vtok = c->dbg_vtok; ca.dbg_vg = c->dbg_vg; ca.dbg_kind = c->dbg_kind; ca.dbg_trig = c->dbg_trig;
+  ca.dbg_out = c->dbg_out;
+  CK(launch_commit(ca, c->st));
+  c->launches++;
+  if (c->timing.on) {
+    cudaEventRecord(tevent(c), c->st);
+    c->timing.rec.emplace_back(ev0, c->timing.used - 1, 2, 0.0);
+  }
+  for (int b = 0; b < B; ++b) {
+    const int s = slots[b];
+    c->pos_h[s] += 1;
+  }
+  for (int i = 0; i < n_gated; ++i) {
+    const int s = slots[rows[i]];
+    c->shadow_h[s] = c->pos_h[s];
+  }
+  c->last_B = B;
+  return MG_OK;
+}
+
+mg_status mg_stats(mg_ctx* c, mg_stats_t* out) {
+  if (!c || !out) return MG_ERR_INVALID;
+  if (c->dead) return fail(c, MG_ERR_CUDA, "context is dead: " + c->err);
+  unsigned long long s[16];
+  int32_t nan = 0;
+  CK(cudaMemcpyAsync(s, c->stats_d, sizeof(s), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(&nan, c->nan_d, 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  out->steps = s[0]; out->rows = s[1]; out->protected_rows = s[2]; out->triggers = s[3];
+  out->verified = s[4]; out->repairs = s[5]; out->verifier_launches = s[6]; out->catchup_tokens = s[7];
+  out->error_flags = nan ? 1u : 0u;
+  return nan ? MG_ERR_NUMERIC : MG_OK;
+}
+
+mg_status mg_release(mg_ctx* c, int32_t slot) {
+  if (!c) return MG_ERR_INVALID;
+  if (slot < 0 || slot >= c->cfg.max_slots) return fail(c, MG_ERR_INVALID, "bad slot");
+  if (!c->active[slot]) return fail(c, MG_ERR_STATE, "slot not active");
+  for (int p : c->pages[slot]) c->free_pages.push_back(p);
+  c->pages[slot].clear();
+  c->active[slot] = 0;
+  c->pos_h[slot] = c->shadow_h[slot] = 0;
+  return MG_OK;
+}
+
+void mg_destroy(mg_ctx* c) {
+  if (!c) return;
+  cudaStreamSynchronize(c->st);
+  for (auto e : c->timing.pool) cudaEventDestroy(e);
+  if (c->stage_ev[0]) cudaEventDestroy(c->stage_ev[0]);
+  if (c->stage_ev[1]) cudaEventDestroy(c->stage_ev[1]);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  delete c;
+}
+
+const char* mg_last_error(const mg_ctx* c) { return c ? c->err.c_str() : g_init_err.c_str(); }
+
+// ================================================================== debug ABI
+mg_status mgd_read_column(mg_ctx* c, int32_t which, int32_t slot, int32_t pos, uint16_t* out) {
+  if (!c || !out || slot < 0 || slot >= c->cfg.max_slots || pos < 0) return MG_ERR_INVALID;
+  if (pos / c->PS >= (int)c->pages[slot].size()) return fail(c, MG_ERR_INVALID, "column not allocated");
+  CK(cudaStreamSynchronize(c->st));
+  const int page = c->pages[slot][pos / c->PS];
+  const uint16_t* pool = which ? c->kv_shadow : c->kv_fast;
+  size_t o = 0;
+  for (int l = 0; l < c->L; ++l)
+    for (int kvsel = 0; kvsel < 2; ++kvsel)
+      for (int h = 0; h < c->KV; ++h) {
+        const size_t off = ((((size_t)l * c->n_pages + page) * 2 + kvsel) * c->KV + h) * (size_t)c->PS * c->hd +
+                           (size_t)(pos % c->PS) * c->hd;
+        CK(cudaMemcpy(out + o, pool + off, c->hd * 2, cudaMemcpyDeviceToHost));
+        o += c->hd;
+      }
+  return MG_OK;
+}
+
+mg_status mgd_cache_digest(mg_ctx* c, int32_t which, int32_t skip_slot, int32_t skip_pos, uint64_t* out) {
+  if (!c || !out) return MG_ERR_INVALID;
+  uint64_t h = 1469598103934665603ull;
+  std::vector<uint16_t> col((size_t)c->L * 2 * c->KV * c->hd);
+  for (int s = 0; s < c->cfg.max_slots; ++s) {
+    if (!c->active[s]) continue;
+    const int n = which ? c->shadow_h[s] : c->pos_h[s];
+    for (int q = 0; q < n; ++q) {
+      if (s == skip_slot && q == skip_pos) continue;
+      mg_status r = mgd_read_column(c, which, s, q, col.data());
+      if (r) return r;
+      for (uint16_t v : col) { h ^= v; h *= 1099511628211ull; }
+    }
+  }
+  *out = h;
+  return MG_OK;
+}
+
+mg_status mgd_last_step(mg_ctx* c, int32_t* f_tok, float* g, float* v1, float* v2, uint8_t* trig, int32_t* v_tok,
+                        float* v_g, uint8_t* kind, int32_t* out) {
+  if (!c) return MG_ERR_INVALID;
+  const int B = c->last_B;
+  CK(cudaStreamSynchronize(c->st));
+  if (f_tok) CK(cudaMemcpy(f_tok, c->f_tok, B * 4, cudaMemcpyDeviceToHost));
+  if (g) CK(cudaMemcpy(g, c->f_g, B * 4, cudaMemcpyDeviceToHost));
+  if (v1) CK(cudaMemcpy(v1, c->f_v1, B * 4, cudaMemcpyDeviceToHost));
+  if (v2) CK(cudaMemcpy(v2, c->f_v2, B * 4, cudaMemcpyDeviceToHost));
+  if (trig) CK(cudaMemcpy(trig, c->dbg_trig, B, cudaMemcpyDeviceToHost));
+  if (v_tok) CK(cudaMemcpy(v_tok, c->dbg_vtok, B * 4, cudaMemcpyDeviceToHost));
+  if (v_g) CK(cudaMemcpy(v_g, c->dbg_vg, B * 4, cudaMemcpyDeviceToHost));
+  if (kind) CK(cudaMemcpy(kind, c->dbg_kind, B, cudaMemcpyDeviceToHost));
+  if (out) CK(cudaMemcpy(out, c->dbg_out, B * 4, cudaMemcpyDeviceToHost));
+  return MG_OK;
+}
+
+mg_status mgd_capture_logits(mg_ctx* c, float* dev_buf) {
+  if (!c) return MG_ERR_INVALID;
+  c->capture = dev_buf;
+  return MG_OK;
+}
+
+mg_status mgd_weight(mg_ctx* c, int32_t layer, int32_t which, uint16_t* out_dev, int64_t* n_host) {
+  // logical (oracle) layout of one tensor, DESIGN.md 3.1
+  if (!c || !n_host) return MG_ERR_INVALID;
+  const uint16_t* src = nullptr;
+  int64_t n = 0;
+  int gu = 0;
+  if (layer < 0) {
+    if (which == 0) { src = c->embed; n = (int64_t)c->V * c->d; }
+    else if (which == 1) { src = c->final_norm; n = c->d; }
+    else { src = c->lm.ptr; n = (int64_t)c->V * c->d; }
+  } else {
+    if (layer >= c->L) return MG_ERR_INVALID;
+    const LayerW& w = c->layers[layer];
+    switch (which) {
+      case 0: src = w.attn_norm; n = c->d; break;
+      case 1: src = w.qkv.ptr; n = (int64_t)c->NQ * c->d; break;
+      case 2: src = w.qkv.ptr + (size_t)c->NQ * c->d; n = (int64_t)c->NK * c->d; break;
+      case 3: src = w.qkv.ptr + (size_t)(c->NQ + c->NK) * c->d; n = (int64_t)c->NK * c->d; break;
+      case 4: src = w.o.ptr; n = (int64_t)c->d * c->NQ; break;
+      case 5: src = w.mlp_norm; n = c->d; break;
+      case 6: case 7: src = w.gu.ptr; n = (int64_t)c->F * c->d; gu = which - 5; break;
+      case 8: src = w.down.ptr; n = (int64_t)c->d * c->F; break;
+      case 9: src = w.bqkv; n = w.bqkv ? c->NQ : 0; break;
+      case 10: src = w.bqkv ? w.bqkv + c->NQ : nullptr; n = w.bqkv ? c->NK : 0; break;
+      case 11: src = w.bqkv ? w.bqkv + c->NQ + c->NK : nullptr; n = w.bqkv ? c->NK : 0; break;
+      default: return MG_ERR_INVALID;
+    }
+  }
+  *n_host = n;
+  if (!out_dev || n == 0) return MG_OK;
+  if (!gu) {
+    CK(cudaMemcpyAsync(out_dev, src, n * 2, cudaMemcpyDeviceToDevice, c->st));
+  } else {
+    for (int j = 0; j < c->F; ++j) {
+      const size_t prow = (size_t)(j / 64) * 128 + (gu == 2 ? 64 : 0) + j % 64;
+      CK(cudaMemcpyAsync(out_dev + (size_t)j * c->d, src + prow * c->d, c->d * 2, cudaMemcpyDeviceToDevice, c->st));
+    }
+  }
+  CK(cudaStreamSynchronize(c->st));
+  return MG_OK;
+}
+
+mg_status mgd_schedule(mg_ctx* c, int32_t T, int32_t det, int32_t max_ctx, int32_t* o) {
+  if (!c || !o || T < 1) return MG_ERR_INVALID;
+  Sched s = det ? sched_det(c, T, max_ctx) : sched_fast(c, T, max_ctx);
+  o[0] = s.qkv.splits; o[1] = s.o.splits; o[2] = s.gu.splits; o[3] = s.down.splits; o[4] = s.lm.splits;
+  o[5] = s.attn_chunk; o[6] = s.qkv.impl; o[7] = s.qkv.mma_n;
+  return MG_OK;
+}
+
+mg_status mgd_launch_count(mg_ctx* c, uint64_t* out) {
+  if (!c || !out) return MG_ERR_INVALID;
+  *out = c->launches;
+  return MG_OK;
+}
+
+mg_status mgd_set_timing(mg_ctx* c, int32_t on) {
+  if (!c) return MG_ERR_INVALID;
+  c->timing.on = on != 0;
+  c->timing.used = 0;
+  c->timing.rec.clear();
+  return MG_OK;
+}
+
+// out: [0] gemm ms total, [1] gemm launches, [2] gemm algorithmic bytes,
+//      [3] attention ms total, [4] attention launches, [5] step ms total, [6] steps
+mg_status mgd_timing(mg_ctx* c, double* out) {
+  if (!c || !out) return MG_ERR_INVALID;
+  CK(cudaStreamSynchronize(c->st));
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  for (auto& r : c->timing.rec) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->timing.pool[std::get<0>(r)], c->timing.pool[std::get<1>(r)]));
+    const int cls = std::get<2>(r);
+    if (cls == 0) { out[0] += ms; out[1] += 1; out[2] += std::get<3>(r); }
+    else if (cls == 1) { out[3] += ms; out[4] += 1; }
+    else { out[5] += ms; out[6] += 1; }
+  }
+  c->timing.used = 0;
+  c->timing.rec.clear();
+  return MG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,112 @@
+// engine.h -- the per-context state of libmargingate (internal).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/mg.h"
+#include "control.h"
+#include "kernels.h"
+
+namespace mg {
+
+struct OpSched {
+  int impl;    // 0 tcgen05, 1 CUDA-core
+  int splits;  // split-K over 64-wide k-blocks
+  int tile_n;  // tokens per CTA (tcgen05)
+  int mma_n;   // tcgen05 instruction N
+};
+struct Sched {
+  OpSched qkv, o, gu, down, lm;
+  int attn_chunk, attn_nch;
+};
+
+struct Weight {
+  uint16_t* ptr = nullptr;
+  int N = 0, K = 0;
+  CUtensorMap map;
+};
+
+struct LayerW {
+  uint16_t *attn_norm, *mlp_norm, *bqkv;
+  Weight qkv, o, gu, down;
+};
+
+struct Timing {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  // pairs: (start idx, stop idx, class)  class 0 gemm, 1 attention, 2 step
+  std::vector<std::tuple<size_t, size_t, int, double>> rec;  // double = algorithmic bytes
+};
+
+}  // namespace mg
+
+struct mg_ctx {
+  mg_config cfg{};
+  mg_buffers buf{};
+  cudaStream_t st = nullptr;
+  std::string err;
+  bool dead = false;
+  int dev = 0;
+
+  // derived shape
+  int L, d, H, KV, hd, F, V, NQ, NK, NQKV;
+  int Tv;     // verifier / prefill chunk (tokens)
+  int Tmax;   // activation rows
+  int PS, max_pages, n_pages;
+  int nb_top2;
+  int nch_max;
+
+  // weights
+  uint16_t *embed, *final_norm;
+  mg::Weight lm;
+  std::vector<mg::LayerW> layers;
+
+  // caches
+  uint16_t *kv_fast, *kv_shadow;
+
+  // workspace
+  uint16_t *x, *xn, *q, *att, *a, *xg, *xgn;
+  float *part, *logits, *attn_acc, *attn_ml, *top2_part;
+  float *rope_cos, *rope_sin;
+  size_t part_elems;
+  // device state
+  int32_t *pos_d, *shadow_d, *hist_d, *pt_d;
+  unsigned long long* stats_d;
+  int32_t* nan_d;
+  // batch / step buffers
+  int32_t *slots_d, *f_slot, *f_pos, *f_tok, *f_nk, *f_i2;
+  uint8_t* prot_d;
+  float *f_g, *f_v1, *f_v2;
+  uint8_t* trig_d;
+  int32_t *rank_d, *ctrl_d, *last_d;
+  int32_t *cu_slot, *cu_pos, *cu_tok, *cu_nk;
+  int32_t *v_tok, *v_i2;
+  float *v_g, *v_v1, *v_v2;
+  int32_t* staging_d;  // uploads: [slots | prot bytes | pt updates]
+  // debug record
+  int32_t *dbg_vtok, *dbg_out;
+  float* dbg_vg;
+  uint8_t *dbg_kind, *dbg_trig;
+  float* capture = nullptr;
+  int last_B = 0;
+
+  // host mirrors
+  std::vector<int> pos_h, shadow_h;
+  std::vector<char> active;
+  std::vector<std::vector<int>> pages;
+  std::vector<int> free_pages;
+  int32_t* pinned = nullptr;  // 2 staging regions + ctrl
+  size_t pinned_words = 0, stage_words = 0;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  int stage_idx = 0;
+
+  std::map<std::tuple<const void*, int, int, int>, CUtensorMap> xmaps;
+  unsigned long long launches = 0;
+  mg::Timing timing;
+};

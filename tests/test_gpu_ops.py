@@ -1,0 +1,205 @@
+"""Per-kernel parity: each CUDA kernel of the hot path vs the oracle on
+identical seeded inputs (SURVEY 8(c) parity protocol, step 1).
+
+Tolerances (BASELINE north_star / DESIGN.md 6):
+  * fp32 GEMM accumulators: |gpu - oracle| <= 1e-5 * sum|x_k w_k|
+  * bf16 outputs: equal or 1 ulp apart (2 ulp where a libm-vs-CUDA expf enters)
+  * weights, top-2, gate, QKV epilogue, residual: bit-exact
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2605_30218_b200 import kernels
+    return kernels
+
+
+def _bf(orc, a):
+    return orc.bf16_to_f32(a).astype(np.float64)
+
+
+def _rand(orc, rng, shape, scale=1.0):
+    return orc.f32_to_bf16((rng.standard_normal(shape) * scale).astype(np.float32))
+
+
+def _ulps(orc, a, b):
+    """|a - b| in units of bf16 ulp of max(|a|,|b|) (bit patterns)."""
+    fa, fb = _bf(orc, a), _bf(orc, b)
+    mag = np.maximum(np.abs(fa), np.abs(fb))
+    ulp = np.where(mag > 0, 2.0 ** (np.floor(np.log2(np.maximum(mag, 1e-38))) - 7), 2.0 ** -133)
+    return np.abs(fa - fb) / ulp
+
+
+# ------------------------------------------------------------------ K0
+@pytest.mark.parametrize("kind,fan", [(0, 4096), (0, 14336), (1, 0), (2, 0), (3, 0)])
+def test_weight_generator_bit_exact(orc, K, kind, fan):
+    n = 1 << 18
+    for tid in (0, 7, 513):
+        assert np.array_equal(K.gen_tensor(42, tid, n, kind, fan), orc.gen_tensor(42, tid, n, kind, fan))
+
+
+# ------------------------------------------------------------------ a2
+@pytest.mark.parametrize("T,d", [(1, 256), (7, 4096), (3, 5120), (2, 3584)])
+def test_rmsnorm(orc, K, T, d):
+    rng = np.random.default_rng(T * d)
+    x = _rand(orc, rng, (T, d), 3.0)
+    w = orc.f32_to_bf16((1 + 0.1 * rng.standard_normal(d)).astype(np.float32))
+    got = K.rmsnorm(x, w, 1e-5)
+    ref = orc.rmsnorm(x, w, 1e-5)
+    assert _ulps(orc, got, ref).max() <= 1.0
+
+
+# ------------------------------------------------------------------ GEMM
+def _check_gemm(orc, x, W, part):
+    xf, Wf = _bf(orc, x), _bf(orc, W)
+    y = part[0].astype(np.float32)
+    for s in range(1, part.shape[0]):
+        y = (y + part[s]).astype(np.float32)
+    ref = orc.gemm(x, W, 1).astype(np.float64)
+    scale = np.abs(xf) @ np.abs(Wf).T
+    err = np.abs(y - ref)
+    assert np.all(np.isfinite(y))
+    assert np.all(err <= 1e-5 * scale + 1e-30), float((err / (scale + 1e-30)).max())
+
+
+@pytest.mark.parametrize("T,N,K_,splits,mma_n,tile_n", [
+    (1, 128, 64, 1, 0, 16), (5, 256, 256, 1, 0, 16), (16, 384, 512, 2, 16, 16), (17, 256, 256, 1, 0, 32),
+    (48, 128, 1024, 3, 16, 48), (64, 512, 4096, 7, 0, 64), (64, 512, 4096, 7, 16, 64), (100, 256, 768, 1, 16, 128),
+    (256, 128, 256, 1, 0, 256), (300, 256, 512, 2, 16, 256), (96, 128, 14336, 16, 32, 96)])
+def test_gemm_tcgen05(orc, K, T, N, K_, splits, mma_n, tile_n):
+    rng = np.random.default_rng(T * 131 + N + K_)
+    x = _rand(orc, rng, (T, K_))
+    W = _rand(orc, rng, (N, K_), 1 / np.sqrt(K_))
+    part = K.gemm(x, W, splits=splits, impl=0, mma_n=mma_n, tile_n=tile_n)
+    assert part.shape == (splits, T, N)
+    _check_gemm(orc, x, W, part)
+    # each split is the dot product over its own contiguous range of 64-wide k-blocks
+    KB = K_ // 64
+    for s in range(splits):
+        lo = (s * (KB // splits) + min(s, KB % splits)) * 64
+        hi = ((s + 1) * (KB // splits) + min(s + 1, KB % splits)) * 64
+        sub = orc.gemm(np.ascontiguousarray(x[:, lo:hi]), np.ascontiguousarray(W[:, lo:hi]), 1)
+        sc = np.abs(_bf(orc, x[:, lo:hi])) @ np.abs(_bf(orc, W[:, lo:hi])).T
+        assert np.all(np.abs(part[s] - sub) <= 1e-5 * sc + 1e-30)
+
+
+@pytest.mark.parametrize("T", [1, 2, 3, 4, 8])
+def test_gemm_cuda_core(orc, K, T):
+    rng = np.random.default_rng(T)
+    x = _rand(orc, rng, (T, 4096))
+    W = _rand(orc, rng, (256, 4096), 1 / 64)
+    for splits in (1, 3):
+        _check_gemm(orc, x, W, K.gemm(x, W, splits=splits, impl=1))
+
+
+def test_gemm_column_invariance(orc, K):
+    """Verifier GEMM (mma_n = 16, fixed split): a token's output is bit-identical
+    whatever other tokens share the launch, wherever its column sits, for any
+    T and tile width (BASELINE north_star: bit-identical at batch 1..B)."""
+    rng = np.random.default_rng(77)
+    N, K_ = 256, 2048
+    W = _rand(orc, rng, (N, K_), 1 / np.sqrt(K_))
+    target = _rand(orc, rng, (1, K_))
+    ref = K.gemm(target, W, splits=4, impl=0, mma_n=16, tile_n=16)[:, 0]
+    for T in (2, 15, 16, 33, 64, 130, 256):
+        others = _rand(orc, rng, (T, K_), 3.0)
+        for col in sorted({0, 1, 15, T // 2, T - 1}):
+            x = others.copy()
+            x[col] = target[0]
+            for tile in sorted({16, 64, 256} | {t for t in (32, 48, 96, 128) if t >= 16}):
+                part = K.gemm(x, W, splits=4, impl=0, mma_n=16, tile_n=tile)
+                assert np.array_equal(part[:, col], ref), (T, col, tile)
+
+
+# ------------------------------------------------------------------ a3 epilogue
+@pytest.mark.parametrize("H,KV,hd,bias,S", [(4, 4, 64, False, 1), (32, 8, 128, False, 3), (28, 4, 128, True, 2)])
+def test_qkv_epilogue_bit_exact(orc, K, H, KV, hd, bias, S):
+    rng = np.random.default_rng(H + KV + S)
+    T = 5
+    N = (H + 2 * KV) * hd
+    part = rng.standard_normal((S, T, N)).astype(np.float32)
+    b = orc.f32_to_bf16((0.02 * rng.standard_normal(N)).astype(np.float32)) if bias else None
+    pos = np.array([0, 1, 17, 640, 4000], np.int32)
+    theta = 1e6 if bias else 5e5
+    q, k, v = K.qkv_epilogue(part, b, pos, H, KV, hd, theta)
+    acc = part[0]
+    for s in range(1, S):
+        acc = (acc + part[s]).astype(np.float32)            # splits summed left to right
+    rq, rk, rv = orc.qkv_epilogue(acc, b, pos, H, KV, hd, theta)
+    assert np.array_equal(q, rq) and np.array_equal(k, rk) and np.array_equal(v, rv)
+
+
+# ------------------------------------------------------------------ a4
+@pytest.mark.parametrize("H,KV,hd,chunk", [(4, 4, 64, 16), (32, 8, 128, 256), (40, 8, 128, 64),
+                                           (28, 4, 128, 512), (32, 8, 128, 100)])
+def test_attention(orc, K, H, KV, hd, chunk):
+    rng = np.random.default_rng(H * hd + chunk)
+    T, stride = 4, 700
+    n_keys = np.array([1, 37, 513, 700], np.int32)
+    q = _rand(orc, rng, (T, H, hd))
+    Kc = _rand(orc, rng, (T, KV, stride, hd))
+    Vc = _rand(orc, rng, (T, KV, stride, hd))
+    o = K.attention(q, Kc, Vc, n_keys, chunk)
+    for t in range(T):
+        ref = orc.attention(q[t], Kc[t], Vc[t], int(n_keys[t]), chunk, 1)
+        assert _ulps(orc, o[t], ref).max() <= 2.0, t
+
+
+# ------------------------------------------------------------------ a5-a7 epilogues
+def test_residual_bit_exact(orc, K):
+    rng = np.random.default_rng(5)
+    T, N, S = 3, 4096, 4
+    x = _rand(orc, rng, (T, N), 4.0)
+    part = rng.standard_normal((S, T, N)).astype(np.float32)
+    got = K.residual(x, part)
+    acc = part[0]
+    for s in range(1, S):
+        acc = (acc + part[s]).astype(np.float32)
+    assert np.array_equal(got, orc.residual(x, acc))
+
+
+def test_swiglu(orc, K):
+    rng = np.random.default_rng(6)
+    T, F, S = 3, 1024, 2
+    part = (4 * rng.standard_normal((S, T, 2 * F))).astype(np.float32)
+    got = K.swiglu(part, F)
+    acc = (part[0] + part[1]).astype(np.float32)
+    # interleaved-by-64 physical layout: row r of tile r//128 is gate if r%128 < 64
+    j = np.arange(F)
+    gcol = (j // 64) * 128 + j % 64
+    ref = orc.swiglu(acc[:, gcol], acc[:, gcol + 64])
+    assert _ulps(orc, got, ref).max() <= 1.0
+
+
+# ------------------------------------------------------------------ a8, a9
+def test_top2_bit_exact(orc, K):
+    rng = np.random.default_rng(8)
+    T, V = 9, 128256
+    L = rng.standard_normal((T, V)).astype(np.float32)
+    L[1, 5] = L[1, 77] = 50.0            # duplicated max -> g = 0, lowest id first
+    L[2, 1000:1010] = 9.0                # ties
+    L[3] = 0.0                           # all equal
+    L[4, 3] = np.nan                     # NaN ranks as -inf, flag set
+    got = K.top2(L)
+    ref = orc.top2(L)
+    for k in ("v1", "i1", "v2", "i2", "g"):
+        assert np.array_equal(got[k], ref[k]), k
+    assert got["nan"] and ref["nan"]
+    assert got["i1"][1] == 5 and got["i2"][1] == 77 and got["g"][1] == 0.0
+    assert got["i1"][3] == 0 and got["i2"][3] == 1
+
+
+def test_gate_exact(orc, K):
+    rng = np.random.default_rng(9)
+    for B in (1, 7, 64, 256):
+        g = np.abs(rng.standard_normal(B)).astype(np.float32)
+        prot = (rng.random(B) < 0.7).astype(np.uint8)
+        for tau in (0.0, 0.3, float(g[0]), 1.0, float("inf")):
+            trig, rows = K.gate(g, prot, tau)
+            ref = orc.gate(g, prot, tau)
+            assert np.array_equal(rows, ref)
+            assert np.array_equal(np.nonzero(trig)[0], ref)
