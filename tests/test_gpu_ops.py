@@ -107,7 +107,7 @@ def test_gemm_column_invariance(orc, K):
     ref = K.gemm(target, W, splits=4, impl=0, mma_n=16, tile_n=16)[:, 0]
     for T in (2, 15, 16, 33, 64, 130, 256):
         others = _rand(orc, rng, (T, K_), 3.0)
-        for col in sorted({0, 1, 15, T // 2, T - 1}):
+        for col in sorted(c for c in {0, 1, 15, T // 2, T - 1} if c < T):
             x = others.copy()
             x[col] = target[0]
             for tile in sorted({16, 64, 256} | {t for t in (32, 48, 96, 128) if t >= 16}):
@@ -144,9 +144,13 @@ def test_attention(orc, K, H, KV, hd, chunk):
     Kc = _rand(orc, rng, (T, KV, stride, hd))
     Vc = _rand(orc, rng, (T, KV, stride, hd))
     o = K.attention(q, Kc, Vc, n_keys, chunk)
+    vmax = float(np.abs(_bf(orc, Vc)).max())
     for t in range(T):
         ref = orc.attention(q[t], Kc[t], Vc[t], int(n_keys[t]), chunk, 1)
-        assert _ulps(orc, o[t], ref).max() <= 2.0, t
+        # 2 bf16 ulp, plus an absolute fp32-reordering slack for outputs that
+        # cancel to ~0 (weighted means of values of size vmax)
+        ok = (_ulps(orc, o[t], ref) <= 2.0) | (np.abs(_bf(orc, o[t]) - _bf(orc, ref)) <= 1e-5 * vmax)
+        assert ok.all(), t
 
 
 # ------------------------------------------------------------------ a5-a7 epilogues
