@@ -27,11 +27,16 @@ mg_status mgd_gen_tensor(uint64_t seed, uint32_t tensor_id, int64_t n, int32_t k
 mg_status mgd_rmsnorm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t d, float eps, uint16_t* out,
                       void* stream);
 
-/* GEMM partials: out[s][t][n] = sum_{k in split s} x[t][k] * W[n][k].
+/* GEMM partials: out[s][t][n] = sum_{k in piece s of n's tile} x[t][k] * W[n][k].
  * impl 0 = tcgen05 (TMA + TMEM), 1 = CUDA-core small-T kernel.
- * splits = split-K count over 64-wide k-blocks; mma_n = tcgen05 instruction N
+ * splits > 0: uniform split-K count over 64-wide k-blocks (piece s = split s);
+ * splits < 0: stream-K over G = -splits virtual CTAs: CTA i owns k-blocks
+ * [i W / G, (i+1) W / G) of the W = (N/128)(K/64) tile-major k-blocks, and
+ * the pieces of tile m are numbered in k order (tcgen05 only);
+ * mma_n = tcgen05 instruction N
  * (16 = the verifier's pinned slot groups, 0 = whole tile); tile_n = tokens
- * per CTA (16..256, multiple of 16; 0 = auto).  N % 128 == 0, K % 64 == 0. */
+ * per CTA (16, 32, 64, 128 or 256; 0 = auto).  N % 128 == 0, K % 64 == 0.
+ * W is row-major [N][K] here; the call tiles it into the engine's layout. */
 mg_status mgd_gemm(const uint16_t* x, const uint16_t* W, int32_t T, int32_t N, int32_t K, int32_t splits,
                    int32_t impl, int32_t mma_n, int32_t tile_n, float* out, void* stream);
 

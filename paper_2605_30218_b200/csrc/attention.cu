@@ -1,42 +1,92 @@
 // attention.cu -- paged GQA decode attention.
 //
-// k_attn_partial: one CTA per (token, kv head, key chunk).  The chunk's keys
-// [c*chunk, min((c+1)*chunk, n_keys)) are read from the paged cache (or a
-// dense buffer in the op-level tests); the G = H/KV query heads that share
-// the kv head are processed together so each K/V byte is read once per
-// token.  Scores: warp w takes keys lo+w, lo+w+4, ...; each lane holds
-// hd/32 dims, fp32 dot + fixed xor-shuffle tree, times fp32(1/sqrt(hd)).
-// Softmax partial per head: m = max, e = expf(s - m), l = fixed-tree sum;
-// acc[d] = sum_j e_j v_j[d] over the chunk's keys in order.
-// k_attn_combine: chunks combined in chunk order with weights expf(m_c - m*),
-// o = bf16(acc / l).
+// k_attn_chunk<HD, NB>: one CTA (4 warps) per (token, kv head, key chunk of
+// 64*NB keys).  The G = H/KV query heads sharing the kv head form the 16-row
+// M side of mma.sync.m16n8k16 tiles (rows >= G are zero), so every K/V byte
+// of the chunk is read from HBM once per token.  Keys come in 16-key blocks
+// (a block never crosses a KV page); warp w owns blocks w, w+4, ...  At kernel
+// start every warp issues ALL its K and V rows as 256-byte cp.async.bulk
+// copies (one mbarrier for K, one for V; rows padded to HD*2+16 bytes so the
+// ldmatrix reads are bank-conflict free), so one HBM round trip per CTA is
+// exposed and the V stream overlaps the score phase.  The chunk follows
+// DESIGN.md 3.3 exactly, in two passes:
+//   pass 1  s_j = (q . k_j) * fp32(1/sqrt(hd))  (bf16 x bf16 products, fp32 acc)
+//   softmax m = max_j s_j, e_j = expf(s_j - m), l = sum_j e_j (fixed trees)
+//   pass 2  acc = sum_j e_j v_j  with e split as bf16 hi + bf16 lo (16+ bit
+//           mantissa) so the probabilities are not rounded to bf16
+// then the 4 warps' partial sums are added in warp order.
+// k_attn_combine: chunks combined in chunk order with weights
+// expf(m_c - m*), o = bf16(acc / l).
 //
-// Schedules: the fast path picks `chunk` from (batch, context) to fill the
-// 148 SMs (the serving shape changes the reduction plan); the
-// verifier always uses a fixed chunk (A14), so a query's result
-// depends only on its own keys.
+// Schedules: the fast path uses 64-key chunks (most CTAs, best at every batch
+// size measured); the verifier uses pinned 128-key chunks (A14), so
+// a query's result depends only on its own keys: the block/warp structure is
+// a function of the chunk bounds alone.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace mg {
 
-constexpr int kAttnThreads = 128;
-constexpr int kAttnCMax = 512;  // max keys per chunk
-constexpr int kAttnGMax = 8;    // max query heads per kv head
+constexpr int kAtThreads = 128;
 
-__global__ void __launch_bounds__(kAttnThreads) k_attn_partial(AttnArgs a) {
-  __shared__ float qs[kAttnGMax][128];
-  __shared__ float sc[kAttnGMax][kAttnCMax];
-  __shared__ float red[4][kAttnGMax];
-  __shared__ float s_m[kAttnGMax], s_l[kAttnGMax];
-  __shared__ float accx[kAttnGMax][64];
+template <int HD, int NB>
+struct AtCfg {
+  static constexpr int ROWB = HD * 2 + 16;
+  static constexpr int BLKB = 16 * ROWB;
+  static constexpr int CH = 64 * NB;                  // keys per chunk
+  static constexpr int S_BYTES = 16 * CH * 4;
+  static constexpr int KV_BYTES = 2 * 4 * NB * BLKB;  // [K|V][warp][NB] blocks
+  static constexpr int X_BYTES = 4 * 16 * HD * 4;     // cross-warp sums, aliases the K/V region
+  static_assert(X_BYTES <= KV_BYTES, "reduction scratch must fit in the K/V region");
+  static constexpr int SMEM = S_BYTES + KV_BYTES + 4 * 16 * 4 + 32 * 4 + 8 * 8;
+};
+
+MG_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+MG_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+MG_DEV void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+MG_DEV void mma_bf16(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int HD, int NB>
+__global__ void __launch_bounds__(kAtThreads) k_attn_chunk(AttnArgs a) {
+  using C = AtCfg<HD, NB>;
+  extern __shared__ __align__(16) uint8_t sm[];
+  float* S = reinterpret_cast<float*>(sm);                                // [16][CH]
+  uint8_t* kvr = sm + C::S_BYTES;                                         // K/V blocks
+  float* red = reinterpret_cast<float*>(sm + C::S_BYTES + C::KV_BYTES);  // [4][16]
+  float* s_ml = red + 4 * 16;                                             // m[16], l[16]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_ml + 32);                // [K 4][V 4]
 
   const int t = blockIdx.x, kvh = blockIdx.y, c = blockIdx.z;
-  const int H = a.H, hd = a.hd, G = a.H / a.KV;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = a.H, G = a.H / a.KV;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  griddep();
   const int n = a.n_keys[t];
-  const int lo = c * a.chunk;
-  const size_t po = ((size_t)t * H + (size_t)kvh * G) * a.n_chunks + c;  // head g: po + g*n_chunks
+  const int lo = c * C::CH;
+  const size_t po = ((size_t)t * H + (size_t)kvh * G) * a.n_chunks + c;
   if (lo >= n) {
     if (threadIdx.x < G) {
       a.part_ml[(po + (size_t)threadIdx.x * a.n_chunks) * 2 + 0] = -INFINITY;
@@ -44,119 +94,176 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_partial(AttnArgs a) {
     }
     return;
   }
-  const int hi = min(n, lo + a.chunk);
+  const int hi = min(n, lo + C::CH);
   const int len = hi - lo;
+  const int nblk = (len + 15) >> 4;
+  const int nbw = nblk > warp ? min(NB, (nblk - warp + 3) >> 2) : 0;  // blocks of this warp
 
-  for (int e = threadIdx.x; e < G * hd; e += kAttnThreads)
-    qs[e / hd][e % hd] = bf2f(a.q[(size_t)t * H * hd + (size_t)kvh * G * hd + e]);
-
-  // K/V row pointer of key j
-  int slot = 0;
-  if (a.paged) slot = a.slot[t];
-  auto krow = [&](int j, int kvsel) -> const uint16_t* {
-    if (a.paged) {
-      const CacheView& cv = a.cache;
-      const int page = cv.pt[(size_t)slot * cv.max_pages + j / cv.page_size];
-      return cv.pool + ((((size_t)cv.layer * cv.n_pages + page) * 2 + kvsel) * cv.kv + kvh) *
-                           (size_t)cv.page_size * hd +
-             (size_t)(j % cv.page_size) * hd;
+  // ---- issue every K and V row of this warp's blocks (one round trip)
+  {
+    const int slot = a.paged ? a.slot[t] : 0;
+    auto krow = [&](int j, int kvsel) -> const uint16_t* {
+      if (a.paged) {
+        const CacheView& cv = a.cache;
+        const int page = cv.pt[(size_t)slot * cv.max_pages + j / cv.page_size];
+        return cv.pool + ((((size_t)cv.layer * cv.n_pages + page) * 2 + kvsel) * cv.kv + kvh) *
+                             (size_t)cv.page_size * HD +
+               (size_t)(j % cv.page_size) * HD;
+      }
+      const uint16_t* base = kvsel ? a.Vd : a.Kd;
+      return base + (((size_t)t * a.KV + kvh) * a.key_stride + j) * HD;
+    };
+    int valid_rows = 0;
+    for (int j = 0; j < nbw; ++j) valid_rows += min(16, hi - (lo + 16 * (warp + 4 * j)));
+    if (lane == 0) {
+      mbar_expect_tx(&bars[warp], (uint32_t)valid_rows * HD * 2);
+      mbar_expect_tx(&bars[4 + warp], (uint32_t)valid_rows * HD * 2);
     }
-    const uint16_t* base = kvsel ? a.Vd : a.Kd;
-    return base + (((size_t)t * a.KV + kvh) * a.key_stride + j) * hd;
-  };
-  __syncthreads();
-
-  const float scale = (float)(1.0 / sqrt((double)hd));
-  // ---- scores
-  if (hd == 128) {
-    for (int j = lo + warp; j < hi; j += 4) {
-      const uint2 kv = *reinterpret_cast<const uint2*>(krow(j, 0) + lane * 4);
-      const float k0 = lo_bf(kv.x), k1 = hi_bf(kv.x), k2 = lo_bf(kv.y), k3 = hi_bf(kv.y);
-      for (int g = 0; g < G; ++g) {
-        const float* qg = &qs[g][lane * 4];
-        float p = qg[0] * k0;
-        p = fmaf(qg[1], k1, p);
-        p = fmaf(qg[2], k2, p);
-        p = fmaf(qg[3], k3, p);
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) p = __fadd_rn(p, __shfl_xor_sync(0xffffffffu, p, off));
-        if (lane == 0) sc[g][j - lo] = __fmul_rn(p, scale);
+    __syncwarp();
+    for (int e = lane; e < nbw * 32; e += 32) {
+      const int j = e >> 5, kvsel = (e >> 4) & 1, r = e & 15;
+      const int key = lo + 16 * (warp + 4 * j) + r;
+      uint8_t* dst = kvr + ((size_t)(kvsel * 4 + warp) * NB + j) * C::BLKB + r * C::ROWB;
+      if (key < hi) {
+        bulk_g2s(dst, krow(key, kvsel), HD * 2, &bars[kvsel * 4 + warp]);
+      } else {
+        for (int q = 0; q < HD / 8; ++q) reinterpret_cast<uint4*>(dst)[q] = make_uint4(0, 0, 0, 0);
       }
     }
-  } else {  // hd == 64
-    for (int j = lo + warp; j < hi; j += 4) {
-      const uint32_t kv = *reinterpret_cast<const uint32_t*>(krow(j, 0) + lane * 2);
-      const float k0 = lo_bf(kv), k1 = hi_bf(kv);
-      for (int g = 0; g < G; ++g) {
-        float p = qs[g][lane * 2] * k0;
-        p = fmaf(qs[g][lane * 2 + 1], k1, p);
+  }
+
+  // ---- Q fragments (A operand, rows = query heads of this kv head, zero-padded)
+  const int r0 = lane >> 2, r1 = r0 + 8, cc = 2 * (lane & 3);
+  const uint16_t* qp = a.q + (size_t)t * H * HD + (size_t)kvh * G * HD;
+  uint32_t qf[HD / 16][4];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) p = __fadd_rn(p, __shfl_xor_sync(0xffffffffu, p, off));
-        if (lane == 0) sc[g][j - lo] = __fmul_rn(p, scale);
+  for (int ks = 0; ks < HD / 16; ++ks) {
+    const int k0 = ks * 16 + cc;
+    qf[ks][0] = r0 < G ? *reinterpret_cast<const uint32_t*>(qp + r0 * HD + k0) : 0u;
+    qf[ks][1] = r1 < G ? *reinterpret_cast<const uint32_t*>(qp + r1 * HD + k0) : 0u;
+    qf[ks][2] = r0 < G ? *reinterpret_cast<const uint32_t*>(qp + r0 * HD + k0 + 8) : 0u;
+    qf[ks][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(qp + r1 * HD + k0 + 8) : 0u;
+  }
+  const float scale = (float)(1.0 / sqrt((double)HD));
+
+  // ---- pass 1: scores
+  __syncwarp();
+  mbar_wait(&bars[warp], 0);
+  for (int j = 0; j < nbw; ++j) {
+    const uint32_t kb = smem_u32(kvr + ((size_t)warp * NB + j) * C::BLKB);
+    const int b = warp + 4 * j;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kg = 0; kg < HD / 32; ++kg) {
+        uint32_t b0, b1, b2, b3;
+        const int mi = lane >> 3, rr = lane & 7;
+        ldsm_x4(kb + (8 * nt + rr) * C::ROWB + (32 * kg + 8 * mi) * 2, b0, b1, b2, b3);
+        mma_bf16(sacc, qf[2 * kg], b0, b1);
+        mma_bf16(sacc, qf[2 * kg + 1], b2, b3);
       }
+      const int j0 = 16 * b + 8 * nt + cc;  // key index within the chunk
+      const bool v0 = lo + j0 < hi, v1 = lo + j0 + 1 < hi;
+      S[r0 * C::CH + j0] = v0 ? __fmul_rn(sacc[0], scale) : -INFINITY;
+      S[r0 * C::CH + j0 + 1] = v1 ? __fmul_rn(sacc[1], scale) : -INFINITY;
+      S[r1 * C::CH + j0] = v0 ? __fmul_rn(sacc[2], scale) : -INFINITY;
+      S[r1 * C::CH + j0 + 1] = v1 ? __fmul_rn(sacc[3], scale) : -INFINITY;
     }
   }
   __syncthreads();
 
-  // ---- softmax partial per head (fixed trees)
-  for (int g = 0; g < G; ++g) {
+  // ---- softmax over the chunk, per query head (fixed trees; rows >= G zeroed)
+  const int nk16 = nblk * 16;
+  for (int g = 0; g < 16; ++g) {
+    if (g >= G) {
+      for (int j = threadIdx.x; j < nk16; j += kAtThreads) S[g * C::CH + j] = 0.f;
+      continue;
+    }
     float m = -INFINITY;
-    for (int j = threadIdx.x; j < len; j += kAttnThreads) m = fmaxf(m, sc[g][j]);
+    for (int j = threadIdx.x; j < len; j += kAtThreads) m = fmaxf(m, S[g * C::CH + j]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if (lane == 0) red[warp][g] = m;
+    if (lane == 0) red[warp * 16 + g] = m;
   }
   __syncthreads();
   if (threadIdx.x < G) {
     const int g = threadIdx.x;
-    s_m[g] = fmaxf(fmaxf(red[0][g], red[1][g]), fmaxf(red[2][g], red[3][g]));
+    s_ml[g] = fmaxf(fmaxf(red[g], red[16 + g]), fmaxf(red[32 + g], red[48 + g]));
   }
   __syncthreads();
   for (int g = 0; g < G; ++g) {
-    const float m = s_m[g];
+    const float m = s_ml[g];
     float l = 0.f;
-    for (int j = threadIdx.x; j < len; j += kAttnThreads) {
-      const float e = expf(__fsub_rn(sc[g][j], m));
-      sc[g][j] = e;
+    for (int j = threadIdx.x; j < nk16; j += kAtThreads) {
+      const float e = j < len ? expf(__fsub_rn(S[g * C::CH + j], m)) : 0.f;
+      S[g * C::CH + j] = e;
       l = __fadd_rn(l, e);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) l = __fadd_rn(l, __shfl_xor_sync(0xffffffffu, l, off));
-    if (lane == 0) red[warp][g] = l;
+    if (lane == 0) red[warp * 16 + g] = l;
   }
   __syncthreads();
   if (threadIdx.x < G) {
     const int g = threadIdx.x;
-    s_l[g] = __fadd_rn(__fadd_rn(red[0][g], red[1][g]), __fadd_rn(red[2][g], red[3][g]));
+    s_ml[16 + g] = __fadd_rn(__fadd_rn(red[g], red[16 + g]), __fadd_rn(red[32 + g], red[48 + g]));
   }
-  // ---- P.V: thread (kg, d) sums keys lo+kg, lo+kg+KG, ... in order
-  const int KG = kAttnThreads / hd;  // 1 (hd 128) or 2 (hd 64)
-  const int kg = threadIdx.x / hd, d = threadIdx.x % hd;
-  float acc[kAttnGMax];
+
+  // ---- pass 2: acc = sum_j e_j v_j  (e = hi + lo, two bf16 MMAs)
+  float acc[HD / 8][4];
 #pragma unroll
-  for (int g = 0; g < kAttnGMax; ++g) acc[g] = 0.f;
-  for (int j = lo + kg; j < hi; j += KG) {
-    const float v = bf2f(krow(j, 1)[d]);
+  for (int nt = 0; nt < HD / 8; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+  mbar_wait(&bars[4 + warp], 0);
+  for (int j = 0; j < nbw; ++j) {
+    const uint32_t vb = smem_u32(kvr + ((size_t)(4 + warp) * NB + j) * C::BLKB);
+    const int j0 = 16 * (warp + 4 * j);
+    uint32_t ph[4], pl[4];
+    {
+      const float* s0 = S + r0 * C::CH + j0 + cc;
+      const float* s1 = S + r1 * C::CH + j0 + cc;
+      const float e[8] = {s0[0], s0[1], s1[0], s1[1], s0[8], s0[9], s1[8], s1[9]};
 #pragma unroll
-    for (int g = 0; g < kAttnGMax; ++g)
-      if (g < G) acc[g] = fmaf(sc[g][j - lo], v, acc[g]);
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t h = pack_bf2(e[2 * q], e[2 * q + 1]);
+        ph[q] = h;
+        pl[q] = pack_bf2(__fsub_rn(e[2 * q], lo_bf(h)), __fsub_rn(e[2 * q + 1], hi_bf(h)));
+      }
+    }
+#pragma unroll
+    for (int n2 = 0; n2 < HD / 16; ++n2) {
+      uint32_t b0, b1, b2, b3;
+      const int mi = lane >> 3, rr = lane & 7;
+      ldsm_x4_t(vb + ((mi & 1) * 8 + rr) * C::ROWB + (16 * n2 + 8 * (mi >> 1)) * 2, b0, b1, b2, b3);
+      mma_bf16(acc[2 * n2], ph, b0, b1);
+      mma_bf16(acc[2 * n2], pl, b0, b1);
+      mma_bf16(acc[2 * n2 + 1], ph, b2, b3);
+      mma_bf16(acc[2 * n2 + 1], pl, b2, b3);
+    }
   }
-  if (KG == 2) {
-    __syncthreads();
-    if (kg == 1)
-      for (int g = 0; g < G; ++g) accx[g][d] = acc[g];
-    __syncthreads();
-    if (kg == 1) return;
-    for (int g = 0; g < G; ++g) acc[g] = __fadd_rn(acc[g], accx[g][d]);
-  } else {
-    __syncthreads();
+  __syncthreads();
+  // ---- add the 4 warps' partial sums in warp order (scratch aliases the K/V blocks)
+  float* X = reinterpret_cast<float*>(kvr);  // [4][16][HD]
+#pragma unroll
+  for (int nt = 0; nt < HD / 8; ++nt) {
+    float* xw = X + (size_t)warp * 16 * HD;
+    xw[r0 * HD + 8 * nt + cc] = acc[nt][0];
+    xw[r0 * HD + 8 * nt + cc + 1] = acc[nt][1];
+    xw[r1 * HD + 8 * nt + cc] = acc[nt][2];
+    xw[r1 * HD + 8 * nt + cc + 1] = acc[nt][3];
   }
-  for (int g = 0; g < G; ++g) {
+  __syncthreads();
+  for (int e = threadIdx.x; e < G * HD; e += kAtThreads) {
+    const int g = e / HD, d = e % HD;
+    float v = X[g * HD + d];
+    v = __fadd_rn(v, X[16 * HD + g * HD + d]);
+    v = __fadd_rn(v, X[32 * HD + g * HD + d]);
+    v = __fadd_rn(v, X[48 * HD + g * HD + d]);
     const size_t o = po + (size_t)g * a.n_chunks;
-    a.part_acc[o * hd + d] = acc[g];
+    a.part_acc[o * HD + d] = v;
     if (d == 0) {
-      a.part_ml[o * 2 + 0] = s_m[g];
-      a.part_ml[o * 2 + 1] = s_l[g];
+      a.part_ml[o * 2 + 0] = s_ml[g];
+      a.part_ml[o * 2 + 1] = s_ml[16 + g];
     }
   }
 }
@@ -165,6 +272,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_attn_partial(AttnArgs a) {
 __global__ void k_attn_combine(const float* __restrict__ part_acc, const float* __restrict__ part_ml,
                                const int32_t* __restrict__ n_keys, int H, int hd, int chunk, int n_chunks,
                                uint16_t* __restrict__ out) {
+  griddep();
   const int t = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   const int nch = (n_keys[t] + chunk - 1) / chunk;
   const size_t base = ((size_t)t * H + h) * n_chunks;
@@ -179,16 +287,39 @@ __global__ void k_attn_combine(const float* __restrict__ part_acc, const float* 
   out[(size_t)t * H * hd + (size_t)h * hd + d] = f2bf(__fdiv_rn(acc, L));
 }
 
+template <int HD, int NB>
+static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_attn_chunk<HD, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         AtCfg<HD, NB>::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return launch_k(k_attn_chunk<HD, NB>, dim3(a.T, a.KV, a.n_chunks), dim3(kAtThreads), AtCfg<HD, NB>::SMEM, st, a);
+}
+
+int attn_max_chunk() { return 256; }
+
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st) {
-  if (a.hd != 64 && a.hd != 128) return cudaErrorInvalidValue;
-  if (a.H / a.KV > kAttnGMax || a.chunk > kAttnCMax || a.chunk < 1) return cudaErrorInvalidValue;
-  dim3 g1(a.T, a.KV, a.n_chunks);
-  k_attn_partial<<<g1, kAttnThreads, 0, st>>>(a);
-  cudaError_t e = cudaGetLastError();
+  if (a.H / a.KV > 16 || a.H % a.KV) return cudaErrorInvalidValue;
+  cudaError_t e;
+  if (a.hd == 128) {
+    if (a.chunk == 64) e = launch_attn_t<128, 1>(a, st);
+    else if (a.chunk == 128) e = launch_attn_t<128, 2>(a, st);
+    else if (a.chunk == 256) e = launch_attn_t<128, 4>(a, st);
+    else return cudaErrorInvalidValue;
+  } else if (a.hd == 64) {
+    if (a.chunk == 64) e = launch_attn_t<64, 1>(a, st);
+    else if (a.chunk == 128) e = launch_attn_t<64, 2>(a, st);
+    else if (a.chunk == 256) e = launch_attn_t<64, 4>(a, st);
+    else return cudaErrorInvalidValue;
+  } else {
+    return cudaErrorInvalidValue;
+  }
   if (e != cudaSuccess) return e;
-  dim3 g2(a.T, a.H);
-  k_attn_combine<<<g2, a.hd, 0, st>>>(a.part_acc, a.part_ml, a.n_keys, a.H, a.hd, a.chunk, a.n_chunks, a.out);
-  return cudaGetLastError();
+  return launch_k(k_attn_combine, dim3(a.T, a.H), dim3(a.hd), 0, st, (const float*)a.part_acc,
+                  (const float*)a.part_ml, a.n_keys, a.H, a.hd, a.chunk, a.n_chunks, a.out);
 }
 
 }  // namespace mg

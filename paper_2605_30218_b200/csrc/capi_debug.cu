@@ -18,7 +18,7 @@ extern "C" {
 mg_status mgd_gen_tensor(uint64_t seed, uint32_t tid, int64_t n, int32_t kind, int32_t fan_in, uint16_t* out,
                          void* stream) {
   if (!out || n < 0 || kind < 0 || kind > 3 || (kind == 0 && fan_in < 1)) return MG_ERR_INVALID;
-  GenSpec g{seed, tid, n, kind, fan_in, 0, 0};
+  GenSpec g{seed, tid, n, kind, fan_in, 0, 0, 0, 0};
   return st_of(launch_gen(g, out, (cudaStream_t)stream));
 }
 
@@ -30,17 +30,40 @@ mg_status mgd_rmsnorm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t d
 
 mg_status mgd_gemm(const uint16_t* x, const uint16_t* W, int32_t T, int32_t N, int32_t K, int32_t splits,
                    int32_t impl, int32_t mma_n, int32_t tile_n, float* out, void* stream) {
-  if (!x || !W || !out || T < 1 || N % 128 || K % 64 || splits < 1 || splits > K / 64) return MG_ERR_INVALID;
+  // splits < 0: stream-K over G = -splits virtual CTAs (tcgen05 only)
+  const int G = splits < 0 ? -splits : 0;
+  if (!x || !W || !out || T < 1 || N % 128 || K % 64 || splits == 0 || splits > K / 64 || G > 4096)
+    return MG_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
-  if (impl == 1) {
-    if (T > 8) return MG_ERR_INVALID;
-    return st_of(launch_gemm_cc(x, W, N, K, T, splits, out, st));
+  if (impl != 1) {
+    if (tile_n <= 0) tile_n = gemm_tile_n(T);
+    if (mma_n < 0 || mma_n > tile_n || (mma_n && tile_n % mma_n) || (mma_n && mma_n % 16)) return MG_ERR_INVALID;
+  } else if (T > 8 || G) {
+    return MG_ERR_INVALID;
   }
-  if (tile_n <= 0) tile_n = gemm_tile_n(T);
-  if (mma_n < 0 || mma_n > tile_n || (mma_n && tile_n % mma_n) || (mma_n && mma_n % 16)) return MG_ERR_INVALID;
-  CUtensorMap mw, mx;
-  if (!make_tmap_2d(&mw, W, K, N, 128) || !make_tmap_2d(&mx, x, K, T, tile_n)) return MG_ERR_CUDA;
-  return st_of(launch_gemm_tc(mw, mx, N, K, T, splits, tile_n, mma_n, out, st));
+  // the kernels read weights in the engine's tiled layout: tile W (row-major here)
+  std::vector<uint16_t> rm((size_t)N * K), tl((size_t)N * K);
+  cudaStreamSynchronize(st);
+  if (cudaMemcpy(rm.data(), W, rm.size() * 2, cudaMemcpyDeviceToHost) != cudaSuccess) return MG_ERR_CUDA;
+  for (size_t r = 0; r < (size_t)N; ++r)
+    for (size_t k = 0; k < (size_t)K; ++k) tl[tiled_offset(r, k, K)] = rm[r * K + k];
+  uint16_t* Wt = nullptr;
+  if (cudaMalloc(&Wt, tl.size() * 2) != cudaSuccess) return MG_ERR_CUDA;
+  cudaMemcpy(Wt, tl.data(), tl.size() * 2, cudaMemcpyHostToDevice);
+  cudaError_t e;
+  if (impl == 1) {
+    e = launch_gemm_cc(x, Wt, N, K, T, splits, out, st);
+  } else {
+    CUtensorMap mw, mx;
+    if (!make_tmap_w_tiled(&mw, Wt, K, N) || !make_tmap_2d(&mx, x, K, T, tile_n)) {
+      cudaFree(Wt);
+      return MG_ERR_CUDA;
+    }
+    e = launch_gemm_tc(mw, mx, N, K, T, G ? 1 : splits, G, tile_n, mma_n, out, st);
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(Wt);
+  return st_of(e);
 }
 
 mg_status mgd_qkv_epilogue(const float* part, int32_t splits, const uint16_t* bias, const int32_t* pos, int32_t T,
@@ -62,7 +85,8 @@ mg_status mgd_qkv_epilogue(const float* part, int32_t splits, const uint16_t* bi
     return MG_ERR_CUDA;
   cudaMemcpy(dc, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(ds, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice);
-  cudaError_t e = launch_epi_qkv(part, splits, bias, pos, T, H, KV, hd, dc, ds, q, nullptr, nullptr, k, v, st);
+  const PartSpec ps{splits, 0, 1, (H + 2 * KV) * hd / 128};
+  cudaError_t e = launch_epi_qkv(part, ps, bias, pos, T, H, KV, hd, dc, ds, q, nullptr, nullptr, k, v, st);
   cudaStreamSynchronize(st);
   cudaFree(dc);
   cudaFree(ds);
@@ -72,7 +96,8 @@ mg_status mgd_qkv_epilogue(const float* part, int32_t splits, const uint16_t* bi
 mg_status mgd_attention(const uint16_t* q, const uint16_t* K, const uint16_t* V, const int32_t* n_keys, int32_t T,
                         int32_t H, int32_t KVh, int32_t hd, int32_t key_stride, int32_t chunk, uint16_t* o,
                         void* stream) {
-  if (!q || !K || !V || !n_keys || !o || T < 1 || chunk < 1 || chunk > 512 || key_stride < 1) return MG_ERR_INVALID;
+  if (!q || !K || !V || !n_keys || !o || T < 1 || chunk < 16 || chunk > 256 || chunk % 16 || key_stride < 1)
+    return MG_ERR_INVALID;
   const int nch = (key_stride + chunk - 1) / chunk;
   float *acc = nullptr, *ml = nullptr;
   if (cudaMalloc(&acc, (size_t)T * H * nch * hd * 4) != cudaSuccess ||
@@ -93,12 +118,12 @@ mg_status mgd_attention(const uint16_t* q, const uint16_t* K, const uint16_t* V,
 mg_status mgd_residual(const uint16_t* x, const float* part, int32_t splits, int32_t T, int32_t N, uint16_t* out,
                        void* stream) {
   if (!x || !part || !out || T < 1 || N < 1 || splits < 1) return MG_ERR_INVALID;
-  return st_of(launch_epi_residual(x, part, splits, T, N, out, (cudaStream_t)stream));
+  return st_of(launch_epi_residual(x, part, PartSpec{splits, 0, 1, 1}, T, N, out, (cudaStream_t)stream));
 }
 
 mg_status mgd_swiglu(const float* part, int32_t splits, int32_t T, int32_t F, uint16_t* out, void* stream) {
   if (!part || !out || T < 1 || F % 64 || splits < 1) return MG_ERR_INVALID;
-  return st_of(launch_epi_swiglu(part, splits, T, F, out, (cudaStream_t)stream));
+  return st_of(launch_epi_swiglu(part, PartSpec{splits, 0, 1, 1}, T, F, out, (cudaStream_t)stream));
 }
 
 mg_status mgd_top2(const float* logits, int32_t T, int32_t V, float* v1, int32_t* i1, float* v2, int32_t* i2,

@@ -29,9 +29,45 @@ __host__ __device__ __forceinline__ int chunk_start(int n, int S, int c) {
 
 MG_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// ------------------------------------------------------------------ split-K partial layout
+// Stream-K partition of W = n_m * KB k-blocks over G virtual CTAs: CTA i owns
+// [floor(i W / G), floor((i+1) W / G)).  owner(w) = CTA that owns k-block w.
+__host__ __device__ __forceinline__ int streamk_owner(long long w, long long W, int G) {
+  return (int)(((w + 1) * G - 1) / W);
+}
+// How many fp32 partial slots hold output feature n (slot p = k order):
+// uniform split-K (G == 0): S; stream-K: pieces of n's 128-feature tile.
+struct PartSpec {
+  int S;   // uniform splits (G == 0)
+  int G;   // stream-K virtual CTAs (0 = uniform)
+  int KB;  // 64-wide k-blocks per tile
+  int n_m; // 128-feature tiles
+};
+__host__ __device__ __forceinline__ int part_count(const PartSpec& p, int n) {
+  if (p.G == 0) return p.S;
+  const long long W = (long long)p.n_m * p.KB;
+  const long long m = n / 128;
+  return streamk_owner((m + 1) * p.KB - 1, W, p.G) - streamk_owner(m * p.KB, W, p.G) + 1;
+}
+
+// ------------------------------------------------------------------ PDL
+// Programmatic dependent launch: every kernel waits for its prerequisite
+// grid before touching data it produced, then lets the next grid launch
+// (trigger only AFTER the wait, so at most one dependent grid is resident
+// early).  Both are no-ops when the kernel was launched without PDL.
+MG_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+MG_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+MG_DEV void griddep() {
+  griddep_wait();
+  griddep_launch();
+}
+
 // ------------------------------------------------------------------ mbarrier
 MG_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+MG_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 MG_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 MG_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -45,6 +81,19 @@ MG_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+// pure spin on test_wait (no suspension): for the single-thread TMA producer
+// and MMA issuer, whose hand-off latency bounds the weight stream
+MG_DEV void mbar_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "SPIN_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra SPIN_%=;\n\t}" ::"r"(a),
       "r"(parity)
       : "memory");
 }
@@ -65,6 +114,21 @@ MG_DEV void tma_load_2d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
       "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+MG_DEV void tma_load_4d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3,
+                             uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+      "%4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
+      : "memory");
+}
+MG_DEV void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 MG_DEV uint64_t policy_evict_first() {

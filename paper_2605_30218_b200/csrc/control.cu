@@ -67,6 +67,7 @@ int top2_blocks(int V) {
 // grid (T, nb), 256 threads; block b scans [b*V/nb, (b+1)*V/nb)
 __global__ void __launch_bounds__(256) k_top2_partial(const float* __restrict__ logits, int V, int nb,
                                                       float* __restrict__ part, int32_t* __restrict__ nan_flag) {
+  griddep();
   __shared__ Top2 sm[8];
   const int t = blockIdx.x, b = blockIdx.y;
   const int lo = chunk_start(V, nb, b), hi = chunk_start(V, nb, b + 1);
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(256) k_top2_partial(const float* __restrict__ 
 
 __global__ void k_top2_final(const float* __restrict__ part, int nb, float* v1, int32_t* i1, float* v2,
                              int32_t* i2, float* g) {
+  griddep();
   const int t = blockIdx.x;
   if (threadIdx.x != 0) return;
   const float* p = part + (size_t)t * nb * 4;
@@ -112,16 +114,15 @@ cudaError_t launch_top2(const float* logits, int T, int V, float* part, int nb, 
                         int32_t* i2, float* g, int32_t* nan_flag, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   dim3 g1(T, nb);
-  k_top2_partial<<<g1, 256, 0, st>>>(logits, V, nb, part, nan_flag);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(k_top2_partial, g1, dim3(256), 0, st, logits, V, nb, part, nan_flag);
   if (e != cudaSuccess) return e;
-  k_top2_final<<<T, 32, 0, st>>>(part, nb, v1, i1, v2, i2, g);
-  return cudaGetLastError();
+  return launch_k(k_top2_final, dim3(T), dim3(32), 0, st, (const float*)part, nb, v1, i1, v2, i2, g);
 }
 
 // ------------------------------------------------------------------ gate
 // Single CTA of 1024 threads (B <= 1024).  Row b = thread b.
 __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
+  griddep();
   __shared__ int wsum[32], wgap[32];
   const int b = threadIdx.x, warp = b >> 5, lane = b & 31;
   const bool valid = b < a.B;
@@ -177,8 +178,7 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
 
 cudaError_t launch_gate(const GateArgs& a, cudaStream_t st) {
   if (a.B > 1024) return cudaErrorInvalidValue;
-  k_gate<<<1, 1024, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(k_gate, dim3(1), dim3(1024), 0, st, a);
 }
 
 // ------------------------------------------------------------------ prepare
@@ -186,6 +186,7 @@ cudaError_t launch_gate(const GateArgs& a, cudaStream_t st) {
 __global__ void k_prepare(const int32_t* __restrict__ slots, int B, const int32_t* __restrict__ pos,
                           const int32_t* __restrict__ hist, int hist_stride, int32_t* f_slot, int32_t* f_pos,
                           int32_t* f_tok, int32_t* f_nk) {
+  griddep();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int s = slots[b], p = pos[s];
@@ -197,8 +198,8 @@ __global__ void k_prepare(const int32_t* __restrict__ slots, int B, const int32_
 
 cudaError_t launch_prepare(const int32_t* slots, int B, const int32_t* pos, const int32_t* hist, int hist_stride,
                            int32_t* f_slot, int32_t* f_pos, int32_t* f_tok, int32_t* f_nk, cudaStream_t st) {
-  k_prepare<<<(B + 127) / 128, 128, 0, st>>>(slots, B, pos, hist, hist_stride, f_slot, f_pos, f_tok, f_nk);
-  return cudaGetLastError();
+  return launch_k(k_prepare, dim3((B + 127) / 128), dim3(128), 0, st, slots, B, pos, hist, hist_stride, f_slot, f_pos,
+                  f_tok, f_nk);
 }
 
 // ------------------------------------------------------------------ column copy
@@ -222,6 +223,7 @@ __device__ __forceinline__ void copy_cols(const ColCopy& c, int slot, int p0, in
 }
 
 __global__ void k_copy_cols(ColCopy c, int slot, int p0, int p1) {
+  griddep();
   copy_cols(c, slot, p0, p1, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
@@ -230,12 +232,12 @@ cudaError_t launch_copy_cols(const ColCopy& c, int slot, int p0, int p1, cudaStr
   const int total = (p1 - p0) * c.L * 2 * c.kv * (c.hd / 8);
   int blocks = (total + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_copy_cols<<<blocks, 256, 0, st>>>(c, slot, p0, p1);
-  return cudaGetLastError();
+  return launch_k(k_copy_cols, dim3(blocks), dim3(256), 0, st, c, slot, p0, p1);
 }
 
 // ------------------------------------------------------------------ commit
 __global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
+  griddep();
   const int b = blockIdx.x;
   const int slot = a.slots[b];
   const int p = a.pos[slot];
@@ -277,13 +279,13 @@ __global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
 }
 
 cudaError_t launch_commit(const CommitArgs& a, cudaStream_t st) {
-  k_commit<<<a.B, 256, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(k_commit, dim3(a.B), dim3(256), 0, st, a);
 }
 
 // prefill bookkeeping: hist[slot][len] = token, pos = shadow_len = len
 __global__ void k_prefill_done(int32_t* hist, int hist_stride, int32_t* pos, int32_t* shadow_len, int slot, int len,
                                const int32_t* tok) {
+  griddep();
   hist[(size_t)slot * hist_stride + len] = tok[0];
   pos[slot] = len;
   shadow_len[slot] = len;
@@ -291,8 +293,7 @@ __global__ void k_prefill_done(int32_t* hist, int hist_stride, int32_t* pos, int
 
 cudaError_t launch_prefill_done(int32_t* hist, int hist_stride, int32_t* pos, int32_t* shadow_len, int slot, int len,
                                 const int32_t* tok, cudaStream_t st) {
-  k_prefill_done<<<1, 1, 0, st>>>(hist, hist_stride, pos, shadow_len, slot, len, tok);
-  return cudaGetLastError();
+  return launch_k(k_prefill_done, dim3(1), dim3(1), 0, st, hist, hist_stride, pos, shadow_len, slot, len, tok);
 }
 
 }  // namespace mg

@@ -4,7 +4,9 @@
 // IEEE fp32 with explicit __fmul_rn/__fadd_rn/__fdiv_rn/__fsqrt_rn (no FMA
 // contraction of the epilogue math), bf16 by round-to-nearest-even.
 // All kernels are per-token: a token's output never depends on which other
-// tokens share the launch (the verifier's batch invariance).
+// tokens share the launch (the verifier's batch invariance).  All are
+// launched with PDL (griddep() first), so the next GEMM's weight prefetch
+// overlaps them.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -25,10 +27,13 @@ __global__ void k_gen(GenSpec g, float c, float offset, uint16_t* __restrict__ d
     const int32_t u = (int32_t)(r >> 40) - 8388608;
     const float v = __fadd_rn(offset, __fmul_rn((float)u, c));
     int64_t o = i;
-    if (g.remap) {  // [gate; up] rows interleaved by 64 inside each 128-row tile
+    if (g.remap || g.tiled || g.row_off) {
       const int64_t row = i / g.row_len, col = i % g.row_len;
-      const int64_t prow = (row / 64) * 128 + (g.remap == 2 ? 64 : 0) + row % 64;
-      o = prow * g.row_len + col;
+      int64_t prow = row;
+      if (g.remap)  // [gate; up] rows interleaved by 64 inside each 128-row tile
+        prow = (row / 64) * 128 + (g.remap == 2 ? 64 : 0) + row % 64;
+      prow += g.row_off;
+      o = g.tiled ? (int64_t)tiled_offset(prow, col, g.row_len) : prow * g.row_len + col;
     }
     dst[o] = f2bf(v);
   }
@@ -52,6 +57,7 @@ cudaError_t launch_gen(const GenSpec& g, uint16_t* dst, cudaStream_t st) {
 // ------------------------------------------------------------------ a1: embed
 __global__ void k_embed(const uint16_t* __restrict__ E, const int32_t* __restrict__ tok, int d,
                         uint16_t* __restrict__ x) {
+  griddep();
   const int t = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(E + (size_t)tok[t] * d);
   uint4* dst = reinterpret_cast<uint4*>(x + (size_t)t * d);
@@ -59,32 +65,15 @@ __global__ void k_embed(const uint16_t* __restrict__ E, const int32_t* __restric
 }
 
 cudaError_t launch_embed(const uint16_t* E, const int32_t* tok, int T, int d, uint16_t* x, cudaStream_t st) {
-  k_embed<<<T, 128, 0, st>>>(E, tok, d, x);
-  return cudaGetLastError();
+  return launch_k(k_embed, dim3(T), dim3(128), 0, st, E, tok, d, x);
 }
 
 // ------------------------------------------------------------------ a2: RMSNorm
 // One CTA (256 threads) per token.  Fixed reduction tree: thread i sums the
-// 8-element vectors i, i+256, ... in order; xor-shuffle tree inside the warp;
-// warp partials summed 0..7 by thread 0.  Same tree at every T.
-__global__ void __launch_bounds__(256) k_rmsnorm(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int d,
-                                                 float eps, uint16_t* __restrict__ out) {
-  __shared__ float red[8];
-  __shared__ float s_inv;
-  const int t = blockIdx.x;
-  const uint4* xv = reinterpret_cast<const uint4*>(x + (size_t)t * d);
-  const int nv = d / 8;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < nv; i += 256) {
-    const uint4 v = xv[i];
-    const uint32_t u[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float a = lo_bf(u[j]), b = hi_bf(u[j]);
-      ss = fmaf(a, a, ss);  // bf16^2 is exact in fp32: fma == mul+add
-      ss = fmaf(b, b, ss);
-    }
-  }
+// squares of the 8-element vectors i, i+256, ... in order; xor-shuffle tree
+// inside the warp; warp partials summed 0..7 by thread 0.  Same tree at every
+// T and in the fused residual variant below (bit-identical results).
+__device__ __forceinline__ float block_inv_rms(float ss, int d, float eps, float* red, float* s_inv) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, off));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -93,37 +82,105 @@ __global__ void __launch_bounds__(256) k_rmsnorm(const uint16_t* __restrict__ x,
     float s = red[0];
     for (int i = 1; i < 8; ++i) s = __fadd_rn(s, red[i]);
     const float mean = __fdiv_rn(s, (float)d);
-    s_inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(mean, eps)));
+    *s_inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(mean, eps)));
   }
   __syncthreads();
-  const float inv = s_inv;
+  return *s_inv;
+}
+
+__device__ __forceinline__ uint4 norm8(uint4 v, uint4 g, float inv) {
+  const uint32_t u[4] = {v.x, v.y, v.z, v.w}, gw[4] = {g.x, g.y, g.z, g.w};
+  uint32_t r[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    r[j] = pack_bf2(__fmul_rn(__fmul_rn(lo_bf(u[j]), inv), lo_bf(gw[j])),
+                    __fmul_rn(__fmul_rn(hi_bf(u[j]), inv), hi_bf(gw[j])));
+  return make_uint4(r[0], r[1], r[2], r[3]);
+}
+
+__device__ __forceinline__ float ss8(uint4 v, float ss) {
+  const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float a = lo_bf(u[j]), b = hi_bf(u[j]);
+    ss = fmaf(a, a, ss);  // bf16^2 is exact in fp32: fma == mul+add
+    ss = fmaf(b, b, ss);
+  }
+  return ss;
+}
+
+__global__ void __launch_bounds__(256) k_rmsnorm(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int d,
+                                                 float eps, uint16_t* __restrict__ out) {
+  __shared__ float red[8];
+  __shared__ float s_inv;
+  griddep();
+  const int t = blockIdx.x;
+  const uint4* xv = reinterpret_cast<const uint4*>(x + (size_t)t * d);
+  const int nv = d / 8;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < nv; i += 256) ss = ss8(xv[i], ss);
+  const float inv = block_inv_rms(ss, d, eps, red, &s_inv);
   const uint4* wv = reinterpret_cast<const uint4*>(w);
   uint4* ov = reinterpret_cast<uint4*>(out + (size_t)t * d);
-  for (int i = threadIdx.x; i < nv; i += 256) {
-    const uint4 v = xv[i], g = __ldg(wv + i);
-    const uint32_t u[4] = {v.x, v.y, v.z, v.w}, gw[4] = {g.x, g.y, g.z, g.w};
-    uint32_t r[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      r[j] = pack_bf2(__fmul_rn(__fmul_rn(lo_bf(u[j]), inv), lo_bf(gw[j])),
-                      __fmul_rn(__fmul_rn(hi_bf(u[j]), inv), hi_bf(gw[j])));
-    ov[i] = make_uint4(r[0], r[1], r[2], r[3]);
-  }
+  for (int i = threadIdx.x; i < nv; i += 256) ov[i] = norm8(xv[i], __ldg(wv + i), inv);
 }
 
 cudaError_t launch_rmsnorm(const uint16_t* x, const uint16_t* w, int T, int d, float eps, uint16_t* out,
                            cudaStream_t st) {
-  k_rmsnorm<<<T, 256, 0, st>>>(x, w, d, eps, out);
-  return cudaGetLastError();
+  return launch_k(k_rmsnorm, dim3(T), dim3(256), 0, st, x, w, d, eps, out);
 }
 
-// ------------------------------------------------------------------ a3 epilogue
+// ------------------------------------------------------------------ a5/a7 (+a2): residual + RMSNorm
+// x <- bf16(x + sum_s part[s]) (splits summed in order), then xn <- RMSNorm(x)
+// with the same fixed tree as k_rmsnorm.  One CTA per token.
 __device__ __forceinline__ float sum_splits(const float* __restrict__ part, int S, size_t stride, size_t idx) {
   float a = part[idx];
   for (int s = 1; s < S; ++s) a = __fadd_rn(a, part[(size_t)s * stride + idx]);
   return a;
 }
 
+__global__ void __launch_bounds__(256) k_residual_norm(uint16_t* __restrict__ x, const float* __restrict__ part,
+                                                       PartSpec ps, int T, int d, const uint16_t* __restrict__ w,
+                                                       float eps, uint16_t* __restrict__ xn) {
+  __shared__ float red[8];
+  __shared__ float s_inv;
+  extern __shared__ uint4 hrow[];  // the new residual row, d/8 vectors
+  griddep();
+  const int t = blockIdx.x;
+  const size_t stride = (size_t)T * d;
+  uint4* xv = reinterpret_cast<uint4*>(x + (size_t)t * d);
+  const int nv = d / 8;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < nv; i += 256) {
+    const uint4 v = xv[i];
+    const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+    uint32_t r[4];
+    const size_t base = (size_t)t * d + (size_t)i * 8;
+    const int S = part_count(ps, i * 8);  // the 8 features share one 128-feature tile
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float a = __fadd_rn(lo_bf(u[j]), sum_splits(part, S, stride, base + 2 * j));
+      const float b = __fadd_rn(hi_bf(u[j]), sum_splits(part, S, stride, base + 2 * j + 1));
+      r[j] = pack_bf2(a, b);
+    }
+    const uint4 h = make_uint4(r[0], r[1], r[2], r[3]);
+    hrow[i] = h;
+    xv[i] = h;
+    ss = ss8(h, ss);
+  }
+  const float inv = block_inv_rms(ss, d, eps, red, &s_inv);
+  if (!xn) return;
+  const uint4* wv = reinterpret_cast<const uint4*>(w);
+  uint4* ov = reinterpret_cast<uint4*>(xn + (size_t)t * d);
+  for (int i = threadIdx.x; i < nv; i += 256) ov[i] = norm8(hrow[i], __ldg(wv + i), inv);
+}
+
+cudaError_t launch_residual_norm(uint16_t* x, const float* part, PartSpec ps, int T, int d, const uint16_t* w,
+                                 float eps, uint16_t* xn, cudaStream_t st) {
+  return launch_k(k_residual_norm, dim3(T), dim3(256), (size_t)d * 2, st, x, part, ps, T, d, w, eps, xn);
+}
+
+// ------------------------------------------------------------------ a3 epilogue
 __device__ __forceinline__ uint16_t* cache_ptr(const CacheView& c, int slot, int pos, int kvsel, int head) {
   const int page = c.pt[(size_t)slot * c.max_pages + pos / c.page_size];
   return c.pool + ((((size_t)c.layer * c.n_pages + page) * 2 + kvsel) * c.kv + head) * (size_t)c.page_size * c.hd +
@@ -131,17 +188,18 @@ __device__ __forceinline__ uint16_t* cache_ptr(const CacheView& c, int slot, int
 }
 
 // grid (T, H + 2KV), block hd/2: thread i owns the rotate-half pair (i, i+hd/2)
-__global__ void k_epi_qkv(const float* __restrict__ part, int S, const uint16_t* __restrict__ bias,
+__global__ void k_epi_qkv(const float* __restrict__ part, PartSpec ps, const uint16_t* __restrict__ bias,
                           const int32_t* __restrict__ pos, int T, int H, int KV, int hd,
                           const float* __restrict__ rcos, const float* __restrict__ rsin, uint16_t* __restrict__ q,
                           CacheView cache, bool paged, const int32_t* __restrict__ slot, uint16_t* __restrict__ kd,
                           uint16_t* __restrict__ vd) {
+  griddep();
   const int t = blockIdx.x, h = blockIdx.y, i = threadIdx.x, h2 = hd / 2;
   const int NQKV = (H + 2 * KV) * hd;
   const size_t stride = (size_t)T * NQKV;
   const int f1 = h * hd + i, f2 = f1 + h2;
-  float a = sum_splits(part, S, stride, (size_t)t * NQKV + f1);
-  float b = sum_splits(part, S, stride, (size_t)t * NQKV + f2);
+  float a = sum_splits(part, part_count(ps, f1), stride, (size_t)t * NQKV + f1);
+  float b = sum_splits(part, part_count(ps, f2), stride, (size_t)t * NQKV + f2);
   if (bias) {
     a = __fadd_rn(a, bf2f(bias[f1]));
     b = __fadd_rn(b, bf2f(bias[f2]));
@@ -173,61 +231,78 @@ __global__ void k_epi_qkv(const float* __restrict__ part, int S, const uint16_t*
   dst[i + h2] = ob;
 }
 
-cudaError_t launch_epi_qkv(const float* part, int S, const uint16_t* bias, const int32_t* pos, int T, int H, int KV,
-                           int hd, const float* rope_cos, const float* rope_sin, uint16_t* q,
+cudaError_t launch_epi_qkv(const float* part, PartSpec ps, const uint16_t* bias, const int32_t* pos, int T, int H,
+                           int KV, int hd, const float* rope_cos, const float* rope_sin, uint16_t* q,
                            const CacheView* cache, const int32_t* slot, uint16_t* k_out, uint16_t* v_out,
                            cudaStream_t st) {
   CacheView cv{};
   if (cache) cv = *cache;
-  dim3 grid(T, H + 2 * KV);
-  k_epi_qkv<<<grid, hd / 2, 0, st>>>(part, S, bias, pos, T, H, KV, hd, rope_cos, rope_sin, q, cv, cache != nullptr,
-                                     slot, k_out, v_out);
-  return cudaGetLastError();
+  const bool paged = cache != nullptr;
+  return launch_k(k_epi_qkv, dim3(T, H + 2 * KV), dim3(hd / 2), 0, st, part, ps, bias, pos, T, H, KV, hd, rope_cos,
+                  rope_sin, q, cv, paged, slot, k_out, v_out);
 }
 
-// ------------------------------------------------------------------ a5/a7: residual
-__global__ void k_epi_residual(const uint16_t* __restrict__ x, const float* __restrict__ part, int S, size_t n,
-                               uint16_t* __restrict__ out) {
+// ------------------------------------------------------------------ residual (op-level tests)
+__global__ void k_epi_residual(const uint16_t* __restrict__ x, const float* __restrict__ part, PartSpec ps, size_t n,
+                               int N, uint16_t* __restrict__ out) {
+  griddep();
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const float a = sum_splits(part, S, n, i);
+    const float a = sum_splits(part, part_count(ps, (int)(i % N)), n, i);
     out[i] = f2bf(__fadd_rn(bf2f(x[i]), a));
   }
 }
 
-cudaError_t launch_epi_residual(const uint16_t* x, const float* part, int S, int T, int N, uint16_t* out,
+cudaError_t launch_epi_residual(const uint16_t* x, const float* part, PartSpec ps, int T, int N, uint16_t* out,
                                 cudaStream_t st) {
   const size_t n = (size_t)T * N;
   size_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_epi_residual<<<(unsigned)blocks, 256, 0, st>>>(x, part, S, n, out);
-  return cudaGetLastError();
+  return launch_k(k_epi_residual, dim3((unsigned)blocks), dim3(256), 0, st, x, part, ps, n, N, out);
 }
 
 // ------------------------------------------------------------------ a6: SwiGLU
-__global__ void k_epi_swiglu(const float* __restrict__ part, int S, int T, int F, uint16_t* __restrict__ out) {
-  const size_t n = (size_t)T * F, stride = (size_t)T * 2 * F;
-  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+// thread per 4 consecutive outputs (same 64-block, so gate/up columns are
+// contiguous float4s)
+__global__ void k_epi_swiglu(const float* __restrict__ part, PartSpec ps, int T, int F, uint16_t* __restrict__ out) {
+  griddep();
+  const size_t n4 = (size_t)T * F / 4, stride = (size_t)T * 2 * F;
+  for (size_t e4 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e4 < n4; e4 += (size_t)gridDim.x * blockDim.x) {
+    const size_t e = e4 * 4;
     const size_t t = e / F;
     const int j = (int)(e % F);
-    const size_t gcol = (size_t)(j / 64) * 128 + (j % 64);
-    const float g = sum_splits(part, S, stride, t * 2 * F + gcol);
-    const float u = sum_splits(part, S, stride, t * 2 * F + gcol + 64);
-    const float den = __fadd_rn(1.0f, expf(-g));
-    out[e] = f2bf(__fmul_rn(__fdiv_rn(g, den), u));
+    const int col = (j / 64) * 128 + (j % 64);  // gate column; up = col + 64 (same 128-feature tile)
+    const int S = part_count(ps, col);
+    const size_t gcol = t * 2 * F + (size_t)col;
+    float4 g = *reinterpret_cast<const float4*>(part + gcol);
+    float4 u = *reinterpret_cast<const float4*>(part + gcol + 64);
+    for (int s = 1; s < S; ++s) {
+      const float4 g2 = *reinterpret_cast<const float4*>(part + (size_t)s * stride + gcol);
+      const float4 u2 = *reinterpret_cast<const float4*>(part + (size_t)s * stride + gcol + 64);
+      g.x = __fadd_rn(g.x, g2.x); g.y = __fadd_rn(g.y, g2.y); g.z = __fadd_rn(g.z, g2.z); g.w = __fadd_rn(g.w, g2.w);
+      u.x = __fadd_rn(u.x, u2.x); u.y = __fadd_rn(u.y, u2.y); u.z = __fadd_rn(u.z, u2.z); u.w = __fadd_rn(u.w, u2.w);
+    }
+    const float gg[4] = {g.x, g.y, g.z, g.w}, uu[4] = {u.x, u.y, u.z, u.w};
+    float a[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float den = __fadd_rn(1.0f, expf(-gg[k]));
+      a[k] = __fmul_rn(__fdiv_rn(gg[k], den), uu[k]);
+    }
+    *reinterpret_cast<uint2*>(out + e) = make_uint2(pack_bf2(a[0], a[1]), pack_bf2(a[2], a[3]));
   }
 }
 
-cudaError_t launch_epi_swiglu(const float* part, int S, int T, int F, uint16_t* out, cudaStream_t st) {
-  const size_t n = (size_t)T * F;
-  size_t blocks = (n + 255) / 256;
+cudaError_t launch_epi_swiglu(const float* part, PartSpec ps, int T, int F, uint16_t* out, cudaStream_t st) {
+  const size_t n4 = (size_t)T * F / 4;
+  size_t blocks = (n4 + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_epi_swiglu<<<(unsigned)blocks, 256, 0, st>>>(part, S, T, F, out);
-  return cudaGetLastError();
+  return launch_k(k_epi_swiglu, dim3((unsigned)blocks), dim3(256), 0, st, part, ps, T, F, out);
 }
 
 // ------------------------------------------------------------------ row gather
 __global__ void k_gather_rows(const uint16_t* __restrict__ src, const int32_t* __restrict__ rows, int sub, int d,
                               uint16_t* __restrict__ dst) {
+  griddep();
   const int i = blockIdx.x;
   const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)(rows[i] - sub) * d);
   uint4* o = reinterpret_cast<uint4*>(dst + (size_t)i * d);
@@ -237,15 +312,13 @@ __global__ void k_gather_rows(const uint16_t* __restrict__ src, const int32_t* _
 cudaError_t launch_gather_rows(const uint16_t* src, const int32_t* rows, int n, int d, uint16_t* dst,
                                cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  k_gather_rows<<<n, 128, 0, st>>>(src, rows, 0, d, dst);
-  return cudaGetLastError();
+  return launch_k(k_gather_rows, dim3(n), dim3(128), 0, st, src, rows, 0, d, dst);
 }
 
 cudaError_t launch_gather_rows_sub(const uint16_t* src, const int32_t* rows, int sub, int n, int d, uint16_t* dst,
                                    cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  k_gather_rows<<<n, 128, 0, st>>>(src, rows, sub, d, dst);
-  return cudaGetLastError();
+  return launch_k(k_gather_rows, dim3(n), dim3(128), 0, st, src, rows, sub, d, dst);
 }
 
 }  // namespace mg

@@ -82,20 +82,39 @@ int splits_for(int N, int K, int T, int tile_n, int impl) {
   return clampi(S, 1, smax < 16 ? smax : 16);
 }
 
+// stream-K virtual CTA count: one per SM, at least 4 k-blocks (256 k) each.
+// A function of the weight shape only (never of the batch).
+int streamk_G(int N, int K) {
+  const int W = (N / 128) * (K / 64);
+  return clampi(W / 4, 1, kSMs);
+}
+
 OpSched op_fast(int N, int K, int T) {
   OpSched o;
+  o.N = N;
+  o.K = K;
   o.impl = T <= 4 ? 1 : 0;
   o.tile_n = gemm_tile_n(T);
   o.mma_n = o.tile_n;
-  o.splits = splits_for(N, K, T, o.tile_n, o.impl);
+  o.splits = o.impl == 1 ? splits_for(N, K, T, o.tile_n, o.impl) : 1;
+  o.G = o.impl == 1 ? 0 : streamk_G(N, K);
   return o;
 }
 OpSched op_det(int N, int K, int T) {
   OpSched o;
+  o.N = N;
+  o.K = K;
   o.impl = 0;
   o.tile_n = gemm_tile_n(T);
-  o.mma_n = 16;                                // pinned 16-column slot groups
-  o.splits = splits_for(N, K, 16, 16, 0);      // depends on the weight shape only
+  o.mma_n = 16;                 // pinned 16-column slot groups
+  o.splits = 1;
+  o.G = streamk_G(N, K);        // partition depends on the weight shape only
+  return o;
+}
+OpSched op_lm(int N, int K, int T, bool det) {  // LM head: no split (top-2 reads whole logits)
+  OpSched o = det ? op_det(N, K, T) : op_fast(N, K, T);
+  o.splits = 1;
+  o.G = 0;
   return o;
 }
 
@@ -107,13 +126,10 @@ static Sched sched_fast(const mg_ctx* c, int T, int max_ctx) {
   s.o = op_fast(c->d, c->NQ, T);
   s.gu = op_fast(2 * c->F, c->d, T);
   s.down = op_fast(c->d, c->F, T);
-  s.lm = op_fast(c->V, c->d, T);
-  s.lm.splits = 1;
-  int nch = clampi(cdiv(2 * kSMs, T * c->KV), 1, 32);
-  int chunk = cdiv(cdiv(max_ctx, nch), 16) * 16;
-  chunk = clampi(chunk, 16, 512);
-  s.attn_chunk = chunk;
-  s.attn_nch = cdiv(max_ctx, chunk);
+  s.lm = op_lm(c->V, c->d, T, false);
+  // 64-key chunks: the most CTAs per (token, kv head), best measured at every batch
+  s.attn_chunk = 64;
+  s.attn_nch = cdiv(max_ctx, 64);
   return s;
 }
 
@@ -123,10 +139,9 @@ static Sched sched_det(const mg_ctx* c, int T, int max_ctx) {
   s.o = op_det(c->d, c->NQ, T);
   s.gu = op_det(2 * c->F, c->d, T);
   s.down = op_det(c->d, c->F, T);
-  s.lm = op_det(c->V, c->d, T);
-  s.lm.splits = 1;
-  s.attn_chunk = 256;
-  s.attn_nch = cdiv(max_ctx, 256);
+  s.lm = op_lm(c->V, c->d, T, true);
+  s.attn_chunk = 128;  // pinned verifier attention split (A14)
+  s.attn_nch = cdiv(max_ctx, 128);
   return s;
 }
 
@@ -181,11 +196,12 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
 
   // GEMM partial buffer: max over ops of S x T x N for the fast (T <= max_batch)
   // and det (T <= Tv) schedules
-  size_t pe = (size_t)g.max_batch * c->V;  // LM logits share the buffer only if larger
+  size_t pe = 0;
   auto upd = [&](const Sched& s, int T) {
-    const size_t v[4] = {(size_t)s.qkv.splits * T * c->NQKV, (size_t)s.o.splits * T * c->d,
-                         (size_t)s.gu.splits * T * 2 * c->F, (size_t)s.down.splits * T * c->d};
-    for (size_t x : v) pe = x > pe ? x : pe;
+    for (const OpSched* o : {&s.qkv, &s.o, &s.gu, &s.down}) {
+      const size_t x = (size_t)part_slots(o->ps(), o->N) * T * o->N;
+      pe = x > pe ? x : pe;
+    }
   };
   for (int T = 1; T <= g.max_batch; ++T) upd(sched_fast(c, T, g.max_seq), T);
   for (int T = 1; T <= c->Tv; T = T < 16 ? T + 1 : T + 16) upd(sched_det(c, T, g.max_seq), T);
@@ -193,8 +209,8 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   c->part_elems = pe;
   c->nch_max = cdiv(g.max_seq, 16);
   if (c->nch_max > 512) c->nch_max = 512;
-  size_t attn_rows_fast = (size_t)g.max_batch * c->H * 33;
-  size_t attn_rows_det = (size_t)c->Tv * c->H * cdiv(g.max_seq, 256);
+  size_t attn_rows_fast = (size_t)g.max_batch * c->H * cdiv(g.max_seq, 64);
+  size_t attn_rows_det = (size_t)c->Tv * c->H * cdiv(g.max_seq, 128);
   size_t attn_rows = attn_rows_fast > attn_rows_det ? attn_rows_fast : attn_rows_det;
 
   Carver s(ws);
@@ -301,12 +317,13 @@ static mg_status gemm(mg_ctx* c, const uint16_t* X, int xrows, int T, const Weig
   } else {
     const CUtensorMap* mx = xmap(c, X, W.K, xrows, o.tile_n);
     if (!mx) return fail(c, MG_ERR_CUDA, "cuTensorMapEncodeTiled failed for activations");
-    CK(launch_gemm_tc(W.map, *mx, W.N, W.K, T, o.splits, o.tile_n, o.mma_n, out, c->st));
+    CK(launch_gemm_tc(W.map, *mx, W.N, W.K, T, o.splits, o.G, o.tile_n, o.mma_n, out, c->st));
   }
   c->launches += 1;
   if (c->timing.on) {
     cudaEventRecord(tevent(c), c->st);
-    const double bytes = (double)W.N * W.K * 2 + (double)T * W.K * 2 + (double)o.splits * T * W.N * 4;
+    // algorithmic bytes: weights once + activations once + one fp32 output per (token, feature)
+    const double bytes = (double)W.N * W.K * 2 + (double)T * W.K * 2 + (double)T * W.N * 4;
     c->timing.rec.emplace_back(i0, i0 + 1, 0, bytes);
   }
   return MG_OK;
@@ -317,15 +334,16 @@ static mg_status gemm(mg_ctx* c, const uint16_t* X, int xrows, int T, const Weig
 static mg_status forward(mg_ctx* c, int T, const int32_t* slot, const int32_t* pos, const int32_t* tok,
                          const int32_t* nk, int which, const Sched& sc) {
   const int Tm = c->Tmax;
+  const float eps = c->cfg.rms_eps;
   CK(launch_embed(c->embed, tok, T, c->d, c->x, c->st));
-  c->launches++;
+  CK(launch_rmsnorm(c->x, c->layers[0].attn_norm, T, c->d, eps, c->xn, c->st));
+  c->launches += 2;
   for (int l = 0; l < c->L; ++l) {
     const LayerW& w = c->layers[l];
-    CK(launch_rmsnorm(c->x, w.attn_norm, T, c->d, c->cfg.rms_eps, c->xn, c->st));
     mg_status r = gemm(c, c->xn, Tm, T, w.qkv, sc.qkv, c->part);
     if (r) return r;
     CacheView cv = cache_view(c, which, l);
-    CK(launch_epi_qkv(c->part, sc.qkv.splits, w.bqkv, pos, T, c->H, c->KV, c->hd, c->rope_cos, c->rope_sin, c->q,
+    CK(launch_epi_qkv(c->part, sc.qkv.ps(), w.bqkv, pos, T, c->H, c->KV, c->hd, c->rope_cos, c->rope_sin, c->q,
                       &cv, slot, nullptr, nullptr, c->st));
     AttnArgs aa{};
     aa.q = c->q; aa.cache = cv; aa.paged = 1; aa.slot = slot; aa.n_keys = nk;
@@ -339,25 +357,25 @@ static mg_status forward(mg_ctx* c, int T, const int32_t* slot, const int32_t* p
       c->timing.rec.emplace_back(i0, i0 + 1, 1, 0.0);
     }
     if ((r = gemm(c, c->att, Tm, T, w.o, sc.o, c->part))) return r;
-    CK(launch_epi_residual(c->x, c->part, sc.o.splits, T, c->d, c->x, c->st));
-    CK(launch_rmsnorm(c->x, w.mlp_norm, T, c->d, c->cfg.rms_eps, c->xn, c->st));
+    CK(launch_residual_norm(c->x, c->part, sc.o.ps(), T, c->d, w.mlp_norm, eps, c->xn, c->st));
     if ((r = gemm(c, c->xn, Tm, T, w.gu, sc.gu, c->part))) return r;
-    CK(launch_epi_swiglu(c->part, sc.gu.splits, T, c->F, c->a, c->st));
+    CK(launch_epi_swiglu(c->part, sc.gu.ps(), T, c->F, c->a, c->st));
     if ((r = gemm(c, c->a, Tm, T, w.down, sc.down, c->part))) return r;
-    CK(launch_epi_residual(c->x, c->part, sc.down.splits, T, c->d, c->x, c->st));
-    c->launches += 8;
+    // residual + the NEXT norm (next layer's attn_norm, or the final norm)
+    const uint16_t* wn = l + 1 < c->L ? c->layers[l + 1].attn_norm : c->final_norm;
+    CK(launch_residual_norm(c->x, c->part, sc.down.ps(), T, c->d, wn, eps, c->xn, c->st));
+    c->launches += 6;
   }
   return MG_OK;
 }
 
-// final norm + LM head + top-2 over rows xin[0..T)
-static mg_status lm_head(mg_ctx* c, const uint16_t* xin, uint16_t* xnorm, int xrows, int T, const OpSched& o,
-                         float* v1, int32_t* i1, float* v2, int32_t* i2, float* g) {
-  CK(launch_rmsnorm(xin, c->final_norm, T, c->d, c->cfg.rms_eps, xnorm, c->st));
+// LM head + top-2 over the final-normed rows xnorm[0..T)
+static mg_status lm_head(mg_ctx* c, const uint16_t* xnorm, int xrows, int T, const OpSched& o, float* v1,
+                         int32_t* i1, float* v2, int32_t* i2, float* g) {
   mg_status r = gemm(c, xnorm, xrows, T, c->lm, o, c->logits);
   if (r) return r;
   CK(launch_top2(c->logits, T, c->V, c->top2_part, c->nb_top2, v1, i1, v2, i2, g, c->nan_d, c->st));
-  c->launches += 3;
+  c->launches += 2;
   return MG_OK;
 }
 
@@ -417,9 +435,9 @@ static mg_status run_det(mg_ctx* c, int M, const std::vector<int>& last_host, in
     int r1 = r0;
     while (r1 < n_last && last_host[r1] < c0 + T) ++r1;
     if (r1 > r0) {
-      CK(launch_gather_rows_sub(c->x, c->last_d + r0, c0, r1 - r0, c->d, c->xg, c->st));
+      CK(launch_gather_rows_sub(c->xn, c->last_d + r0, c0, r1 - r0, c->d, c->xgn, c->st));
       c->launches++;
-      if ((r = lm_head(c, c->xg, c->xgn, c->cfg.max_batch, r1 - r0, sc.lm, c->v_v1 + r0, c->v_tok + r0,
+      if ((r = lm_head(c, c->xgn, c->cfg.max_batch, r1 - r0, sc.lm, c->v_v1 + r0, c->v_tok + r0,
                        c->v_v2 + r0, c->v_i2 + r0, c->v_g + r0)))
         return r;
     }
@@ -453,25 +471,27 @@ static mg_status gen_weights(mg_ctx* c) {
     if (layer < 0) return which == 0 ? 0u : (uint32_t)(1 + 16 * L + (which - 1));
     return (uint32_t)(1 + 16 * layer + which);
   };
-  auto gen = [&](uint32_t t, int64_t n, int kind, int fan, uint16_t* dst, int remap = 0, int row_len = 0) {
-    GenSpec g{seed, t, n, kind, fan, row_len, remap};
+  auto gen = [&](uint32_t t, int64_t n, int kind, int fan, uint16_t* dst, int remap = 0, int row_len = 0,
+                 int row_off = 0, int tiled = 0) {
+    GenSpec g{seed, t, n, kind, fan, row_len, remap, row_off, tiled};
     c->launches++;
     return launch_gen(g, dst, c->st);
   };
-  CK(gen(tid(-1, 0), (int64_t)c->V * c->d, 1, 0, c->embed));
-  CK(gen(tid(-1, 1), c->d, 2, 0, c->final_norm));
-  CK(gen(tid(-1, 2), (int64_t)c->V * c->d, 0, c->d, c->lm.ptr));
+  const int d = c->d;
+  CK(gen(tid(-1, 0), (int64_t)c->V * d, 1, 0, c->embed));
+  CK(gen(tid(-1, 1), d, 2, 0, c->final_norm));
+  CK(gen(tid(-1, 2), (int64_t)c->V * d, 0, d, c->lm.ptr, 0, d, 0, 1));
   for (int l = 0; l < L; ++l) {
     LayerW& w = c->layers[l];
-    CK(gen(tid(l, 0), c->d, 2, 0, w.attn_norm));
-    CK(gen(tid(l, 1), (int64_t)c->NQ * c->d, 0, c->d, w.qkv.ptr));
-    CK(gen(tid(l, 2), (int64_t)c->NK * c->d, 0, c->d, w.qkv.ptr + (size_t)c->NQ * c->d));
-    CK(gen(tid(l, 3), (int64_t)c->NK * c->d, 0, c->d, w.qkv.ptr + (size_t)(c->NQ + c->NK) * c->d));
-    CK(gen(tid(l, 4), (int64_t)c->d * c->NQ, 0, c->NQ, w.o.ptr));
-    CK(gen(tid(l, 5), c->d, 2, 0, w.mlp_norm));
-    CK(gen(tid(l, 6), (int64_t)c->F * c->d, 0, c->d, w.gu.ptr, 1, c->d));
-    CK(gen(tid(l, 7), (int64_t)c->F * c->d, 0, c->d, w.gu.ptr, 2, c->d));
-    CK(gen(tid(l, 8), (int64_t)c->d * c->F, 0, c->F, w.down.ptr));
+    CK(gen(tid(l, 0), d, 2, 0, w.attn_norm));
+    CK(gen(tid(l, 1), (int64_t)c->NQ * d, 0, d, w.qkv.ptr, 0, d, 0, 1));
+    CK(gen(tid(l, 2), (int64_t)c->NK * d, 0, d, w.qkv.ptr, 0, d, c->NQ, 1));
+    CK(gen(tid(l, 3), (int64_t)c->NK * d, 0, d, w.qkv.ptr, 0, d, c->NQ + c->NK, 1));
+    CK(gen(tid(l, 4), (int64_t)d * c->NQ, 0, c->NQ, w.o.ptr, 0, c->NQ, 0, 1));
+    CK(gen(tid(l, 5), d, 2, 0, w.mlp_norm));
+    CK(gen(tid(l, 6), (int64_t)c->F * d, 0, d, w.gu.ptr, 1, d, 0, 1));
+    CK(gen(tid(l, 7), (int64_t)c->F * d, 0, d, w.gu.ptr, 2, d, 0, 1));
+    CK(gen(tid(l, 8), (int64_t)d * c->F, 0, c->F, w.down.ptr, 0, c->F, 0, 1));
     if (w.bqkv) {
       CK(gen(tid(l, 9), c->NQ, 3, 0, w.bqkv));
       CK(gen(tid(l, 10), c->NK, 3, 0, w.bqkv + c->NQ));
@@ -529,8 +549,8 @@ mg_status mg_init(const mg_config* cfg, const mg_buffers* bufs, void* stream, mg
   // tensor maps of the weights (box: 64 k x 128 rows)
   for (auto& l : c->layers)
     for (Weight* w : {&l.qkv, &l.o, &l.gu, &l.down})
-      if (!make_tmap_2d(&w->map, w->ptr, w->K, w->N, 128)) return die("cuTensorMapEncodeTiled failed (weights)");
-  if (!make_tmap_2d(&c->lm.map, c->lm.ptr, c->lm.K, c->lm.N, 128)) return die("cuTensorMapEncodeTiled failed (lm)");
+      if (!make_tmap_w_tiled(&w->map, w->ptr, w->K, w->N)) return die("cuTensorMapEncodeTiled failed (weights)");
+  if (!make_tmap_w_tiled(&c->lm.map, c->lm.ptr, c->lm.K, c->lm.N)) return die("cuTensorMapEncodeTiled failed (lm)");
 
   std::vector<float> cs, sn;
   init_rope(c->cfg, cs, sn);
@@ -654,7 +674,7 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
   Sched fs = sched_fast(c, B, max_ctx);
   mg_status r = forward(c, B, c->f_slot, c->f_pos, c->f_tok, c->f_nk, 0, fs);
   if (r) return r;
-  if ((r = lm_head(c, c->x, c->xn, c->Tmax, B, fs.lm, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g))) return r;
+  if ((r = lm_head(c, c->xn, c->Tmax, B, fs.lm, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g))) return r;
   if (c->capture) CK(cudaMemcpyAsync(c->capture, c->logits, (size_t)B * c->V * 4, cudaMemcpyDeviceToDevice, c->st));
 
   // 3. gate (+ 4. verifier)
@@ -816,25 +836,29 @@ mg_status mgd_capture_logits(mg_ctx* c, float* dev_buf) {
 mg_status mgd_weight(mg_ctx* c, int32_t layer, int32_t which, uint16_t* out_dev, int64_t* n_host) {
   // logical (oracle) layout of one tensor, DESIGN.md 3.1
   if (!c || !n_host) return MG_ERR_INVALID;
+  // GEMM weights are stored tiled (tiled_offset) with [gate;up] interleaved by
+  // 64 rows and q|k|v fused: undo both on the host.
   const uint16_t* src = nullptr;
   int64_t n = 0;
-  int gu = 0;
+  int gu = 0, row_off = 0, K = 0, rows_total = 0;  // K > 0: tiled GEMM weight
   if (layer < 0) {
     if (which == 0) { src = c->embed; n = (int64_t)c->V * c->d; }
     else if (which == 1) { src = c->final_norm; n = c->d; }
-    else { src = c->lm.ptr; n = (int64_t)c->V * c->d; }
+    else { src = c->lm.ptr; n = (int64_t)c->V * c->d; K = c->d; rows_total = c->V; }
   } else {
     if (layer >= c->L) return MG_ERR_INVALID;
     const LayerW& w = c->layers[layer];
     switch (which) {
       case 0: src = w.attn_norm; n = c->d; break;
-      case 1: src = w.qkv.ptr; n = (int64_t)c->NQ * c->d; break;
-      case 2: src = w.qkv.ptr + (size_t)c->NQ * c->d; n = (int64_t)c->NK * c->d; break;
-      case 3: src = w.qkv.ptr + (size_t)(c->NQ + c->NK) * c->d; n = (int64_t)c->NK * c->d; break;
-      case 4: src = w.o.ptr; n = (int64_t)c->d * c->NQ; break;
+      case 1: src = w.qkv.ptr; n = (int64_t)c->NQ * c->d; K = c->d; rows_total = c->NQKV; break;
+      case 2: src = w.qkv.ptr; n = (int64_t)c->NK * c->d; K = c->d; rows_total = c->NQKV; row_off = c->NQ; break;
+      case 3:
+        src = w.qkv.ptr; n = (int64_t)c->NK * c->d; K = c->d; rows_total = c->NQKV; row_off = c->NQ + c->NK;
+        break;
+      case 4: src = w.o.ptr; n = (int64_t)c->d * c->NQ; K = c->NQ; rows_total = c->d; break;
       case 5: src = w.mlp_norm; n = c->d; break;
-      case 6: case 7: src = w.gu.ptr; n = (int64_t)c->F * c->d; gu = which - 5; break;
-      case 8: src = w.down.ptr; n = (int64_t)c->d * c->F; break;
+      case 6: case 7: src = w.gu.ptr; n = (int64_t)c->F * c->d; gu = which - 5; K = c->d; rows_total = 2 * c->F; break;
+      case 8: src = w.down.ptr; n = (int64_t)c->d * c->F; K = c->F; rows_total = c->d; break;
       case 9: src = w.bqkv; n = w.bqkv ? c->NQ : 0; break;
       case 10: src = w.bqkv ? w.bqkv + c->NQ : nullptr; n = w.bqkv ? c->NK : 0; break;
       case 11: src = w.bqkv ? w.bqkv + c->NQ + c->NK : nullptr; n = w.bqkv ? c->NK : 0; break;
@@ -843,13 +867,17 @@ mg_status mgd_weight(mg_ctx* c, int32_t layer, int32_t which, uint16_t* out_dev,
   }
   *n_host = n;
   if (!out_dev || n == 0) return MG_OK;
-  if (!gu) {
+  if (!K) {
     CK(cudaMemcpyAsync(out_dev, src, n * 2, cudaMemcpyDeviceToDevice, c->st));
   } else {
-    for (int j = 0; j < c->F; ++j) {
-      const size_t prow = (size_t)(j / 64) * 128 + (gu == 2 ? 64 : 0) + j % 64;
-      CK(cudaMemcpyAsync(out_dev + (size_t)j * c->d, src + prow * c->d, c->d * 2, cudaMemcpyDeviceToDevice, c->st));
+    std::vector<uint16_t> phys((size_t)rows_total * K), logical((size_t)n);
+    CK(cudaMemcpy(phys.data(), src, phys.size() * 2, cudaMemcpyDeviceToHost));
+    const int64_t rows = n / K;
+    for (int64_t j = 0; j < rows; ++j) {
+      const size_t prow = gu ? (size_t)(j / 64) * 128 + (gu == 2 ? 64 : 0) + j % 64 : (size_t)(j + row_off);
+      for (int k = 0; k < K; ++k) logical[(size_t)j * K + k] = phys[tiled_offset(prow, k, K)];
     }
+    CK(cudaMemcpy(out_dev, logical.data(), logical.size() * 2, cudaMemcpyHostToDevice));
   }
   CK(cudaStreamSynchronize(c->st));
   return MG_OK;
@@ -858,7 +886,8 @@ mg_status mgd_weight(mg_ctx* c, int32_t layer, int32_t which, uint16_t* out_dev,
 mg_status mgd_schedule(mg_ctx* c, int32_t T, int32_t det, int32_t max_ctx, int32_t* o) {
   if (!c || !o || T < 1) return MG_ERR_INVALID;
   Sched s = det ? sched_det(c, T, max_ctx) : sched_fast(c, T, max_ctx);
-  o[0] = s.qkv.splits; o[1] = s.o.splits; o[2] = s.gu.splits; o[3] = s.down.splits; o[4] = s.lm.splits;
+  auto sp = [](const OpSched& x) { return x.G > 0 ? -x.G : x.splits; };  // < 0: stream-K over -v CTAs
+  o[0] = sp(s.qkv); o[1] = sp(s.o); o[2] = sp(s.gu); o[3] = sp(s.down); o[4] = sp(s.lm);
   o[5] = s.attn_chunk; o[6] = s.qkv.impl; o[7] = s.qkv.mma_n;
   return MG_OK;
 }

@@ -16,7 +16,10 @@ namespace mg {
 
 struct OpSched {
   int impl;    // 0 tcgen05, 1 CUDA-core
-  int splits;  // split-K over 64-wide k-blocks
+  int splits;  // uniform split-K over 64-wide k-blocks (G == 0)
+  int G;       // stream-K virtual CTAs per token tile (0 = uniform split-K)
+  int N, K;    // weight shape (for the partial layout)
+  PartSpec ps() const { return PartSpec{splits, G, K / 64, N / 128}; }
   int tile_n;  // tokens per CTA (tcgen05)
   int mma_n;   // tcgen05 instruction N
 };

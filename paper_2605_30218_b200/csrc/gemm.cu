@@ -1,21 +1,32 @@
 // gemm.cu -- weight-streaming GEMM partials for the decode path (SURVEY 8(a)
-// rows a3, a5-a8): out[s][t][n] = sum_{k in split s} x[t][k] * W[n][k].
+// rows a3, a5-a8): out[s][t][n] = sum_{k in piece s} x[t][k] * W[n][k].
 //
-// k_gemm_tc: tcgen05 "swap-AB" kernel.  The weight tile (128 output
-// features x 64 k, K-major, 128B-swizzled) is the MMA M operand, the
-// tokens (TN x 64) the N operand; both are staged by TMA through an
-// NS-deep mbarrier ring; one elected thread issues tcgen05.mma into a fp32
-// TMEM accumulator (128 lanes x TN columns); all four warps drain TMEM with
-// tcgen05.ld and write the split's fp32 partial.  The split-K reduction and
-// the op's epilogue (bias/RoPE/append, residual, SwiGLU, top-2) run in the
-// consumer kernels in split order, so the result is run-to-run
-// deterministic (no float atomics).
+// k_gemm_tc: persistent, warp-specialised tcgen05 "swap-AB" kernel.
+//   Work piece = (128 output features, a contiguous range of 64-wide
+//   k-blocks, one tile of <= TN tokens); pieces come from a stream-K
+//   partition over G virtual CTAs (or a uniform split-K), so every SM streams
+//   the same number of weight bytes.
+//   warp 0     TMA producer: weight boxes (128 x 64, tiled layout = one
+//              contiguous 16 KB each, 128B swizzle) are the MMA M operand, the
+//              TN tokens x 64 the N operand; KS k-blocks per stage behind one
+//              mbarrier, NS stages, a ring that never drains between pieces;
+//   warp 1     tcgen05.mma (M128 x N x K16, bf16 -> fp32) into one of two TMEM
+//              accumulators (double buffered), issued by one lane of a
+//              warp-uniform loop with precomputed descriptors (the issue
+//              loop, not HBM, was the measured bottleneck of a per-lane loop);
+//   warps 2-5  epilogue: tcgen05.ld the accumulator, write the piece's fp32
+//              partial, release the TMEM buffer.
+//   PDL: before griddepcontrol.wait the producer already streams the first
+//   stages' weights (weights never depend on the previous kernel).
+// The split-K reduction and the op's epilogue (bias/RoPE/append, residual,
+// SwiGLU, top-2) run in the consumer kernels in k order, so results are
+// run-to-run deterministic (no float atomics).
 //
-// Batch invariance (BASELINE north_star, A14): the verifier calls
-// this kernel with a split count fixed per weight shape and mma_n = 16, i.e.
-// every token column is produced by an M128 x N16 x K16 instruction sequence
-// over the same k-blocks in the same order whatever the batch; the fast path
-// may use mma_n = TN (one instruction for the whole tile).
+// Batch invariance (BASELINE north_star, A14): the verifier uses a
+// partition fixed per weight shape and MMA16 (every token column produced by
+// M128 x N16 x K16 instructions over the same k-blocks in the same order,
+// whatever the batch); tested bit-exact in
+// tests/test_gpu_ops.py::test_gemm_column_invariance.
 //
 // k_gemm_cc: CUDA-core kernel for T <= 8 tokens (the fast path's tiny-batch
 // choice): warp per output row, 128-bit weight loads, fp32 FMA, fixed
@@ -23,39 +34,115 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef MG_GEMM_SMEM_KB
+#define MG_GEMM_SMEM_KB 192  // smem ring budget per CTA
+#endif
+#ifndef MG_GEMM_NS_MAX
+#define MG_GEMM_NS_MAX 8
+#endif
+#ifndef MG_GEMM_KS
+#define MG_GEMM_KS 2
+#endif
+
 namespace mg {
+
+int g_pdl = 1;
+int g_gemm_dbg = 0;  // microbenchmark knobs (scripts/gemm_bench.cu); always 0 in the library
 
 template <int TN>
 struct GemmTcCfg {
   static constexpr int BM = 128, BK = 64;
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = TN * BK * 2;
+  static constexpr int KS = MG_GEMM_KS;      // 64-wide k-blocks per pipeline stage
+  static constexpr int A_BOX = BM * BK * 2;  // one TMA box (16 KB, contiguous in HBM)
+  static constexpr int B_BOX = TN * BK * 2;
+  static constexpr int A_BYTES = KS * A_BOX;
+  static constexpr int B_BYTES = KS * B_BOX;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int NS0 = (192 * 1024) / STAGE;
-  static constexpr int NS = NS0 > 8 ? 8 : NS0;
-  static constexpr int TMEM_COLS = TN <= 32 ? 32 : (TN <= 64 ? 64 : (TN <= 128 ? 128 : 256));
-  static constexpr int SMEM = 1024 + NS * STAGE + (2 * NS + 2) * 8 + 16;
+  static constexpr int NS0 = (MG_GEMM_SMEM_KB * 1024) / STAGE;
+  static constexpr int NS = NS0 > MG_GEMM_NS_MAX ? MG_GEMM_NS_MAX : NS0;
+  static constexpr int ACC_COLS = TN < 32 ? 32 : TN;
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;
+  static constexpr int THREADS = 192;
+  static constexpr int SMEM = 1024 + NS * STAGE + (2 * NS + 4) * 8 + 16;
+  static_assert(NS >= 2, "pipeline needs two stages");
 };
 
-template <int TN>
-__global__ void __launch_bounds__(128, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, int N, int K,
-              int T, int splits, int mma_n, float* __restrict__ out) {
+struct GemmArgs {
+  int N, K, T, splits;
+  int n_m, n_t, units;
+  int G;    // > 0: stream-K over G virtual CTAs per token tile; 0: uniform split-K
+  int dbg;  // microbenchmark knobs (0 in the product): 1 skip MMAs, 2 skip stores, 1024 trace CTA 0
+  float* out;
+};
+
+// A piece = one contiguous k-block range of one 128-feature tile for one
+// token tile; its fp32 partial goes to out[slot].  Every role of the CTA
+// walks the same piece sequence.
+struct Piece {
+  int mt, kb0, kb1, slot, tt;
+};
+struct PieceIter {
+  int KB, n_m, n_t, S, G, units;
+  long long W, w, w1;
+  int v, i, tt, u;
+  __device__ explicit PieceIter(const GemmArgs& g, int KB_) {
+    KB = KB_; n_m = g.n_m; n_t = g.n_t; S = g.splits; G = g.G; units = g.units;
+    W = (long long)n_m * KB;
+    u = blockIdx.x;
+    v = (int)blockIdx.x - (int)gridDim.x;
+    w = w1 = 0;
+    i = tt = 0;
+  }
+  __device__ bool next(Piece& p) {
+    if (G == 0) {
+      if (u >= units) return false;
+      p.tt = u % n_t;
+      const int r = u / n_t;
+      p.slot = r % S;
+      p.mt = r / S;
+      p.kb0 = chunk_start(KB, S, p.slot);
+      p.kb1 = chunk_start(KB, S, p.slot + 1);
+      u += gridDim.x;
+      return true;
+    }
+    while (w >= w1) {
+      v += gridDim.x;
+      if (v >= G * n_t) return false;
+      tt = v / G;
+      i = v % G;
+      w = (long long)i * W / G;
+      w1 = (long long)(i + 1) * W / G;
+    }
+    p.tt = tt;
+    p.mt = (int)(w / KB);
+    p.kb0 = (int)(w % KB);
+    p.kb1 = (int)min((long long)KB, p.kb0 + (w1 - w));
+    p.slot = i - streamk_owner((long long)p.mt * KB, W, G);
+    w += p.kb1 - p.kb0;
+    return true;
+  }
+};
+
+template <int TN, bool MMA16>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, GemmArgs g) {
   using C = GemmTcCfg<TN>;
+  constexpr int KS = C::KS;
+  constexpr int MN = MMA16 ? 16 : TN;  // instruction N
+  constexpr int NG = TN / MN;          // instructions per k-step
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::NS * C::A_BYTES;
   uint64_t* full = (uint64_t*)(sB + C::NS * C::B_BYTES);
   uint64_t* empty = full + C::NS;
-  uint64_t* accf = empty + C::NS;
-  uint32_t* tmem_slot = (uint32_t*)(accf + 1);
+  uint64_t* tfull = empty + C::NS;  // [2]
+  uint64_t* tempty = tfull + 2;     // [2]
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * C::BM, t0 = blockIdx.y * TN, s = blockIdx.z;
-  const int KB = K / C::BK;
-  const int kb0 = chunk_start(KB, splits, s), kb1 = chunk_start(KB, splits, s + 1);
-  const int nkb = kb1 - kb0;
+  const int KB = g.K / C::BK;
+  long long* trace = ((g.dbg & 1024) && blockIdx.x == 0) ? reinterpret_cast<long long*>(g.out) : nullptr;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&mapW);
@@ -64,7 +151,10 @@ __global__ void __launch_bounds__(128, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(accf, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);  // one arrival per epilogue warp
+    }
     fence_mbar_init();
   }
   if (warp == 2) tc_alloc(tmem_slot, C::TMEM_COLS);
@@ -73,62 +163,125 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  Piece pc;
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
-      const uint64_t pol = policy_evict_first();  // weights are streamed once
-      for (int i = 0; i < nkb; ++i) {
-        const int st = i % C::NS;
-        const uint32_t ph = (uint32_t)(i / C::NS) & 1u;
-        mbar_wait(&empty[st], ph ^ 1u);
-        mbar_expect_tx(&full[st], C::STAGE);
-        tma_load_2d_hint(sA + st * C::A_BYTES, &mapW, &full[st], (kb0 + i) * C::BK, m0, pol);
-        tma_load_2d(sB + st * C::B_BYTES, &mapX, &full[st], (kb0 + i) * C::BK, t0);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer (single thread)
-      const uint32_t idesc = umma_idesc_bf16(128, mma_n);
-      const int ngroups = TN / mma_n;
-      for (int i = 0; i < nkb; ++i) {
-        const int st = i % C::NS;
-        const uint32_t ph = (uint32_t)(i / C::NS) & 1u;
-        mbar_wait(&full[st], ph);
-        tc_fence_after();
-        const uint32_t a_addr = smem_u32(sA + st * C::A_BYTES);
-        const uint32_t b_addr = smem_u32(sB + st * C::B_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < C::BK / 16; ++kk) {
-          const uint64_t ad = umma_desc_sw128(a_addr + kk * 32);
-          for (int g = 0; g < ngroups; ++g) {
-            const uint64_t bd = umma_desc_sw128(b_addr + g * mma_n * 128 + kk * 32);
-            tc_mma_bf16(tmem + (uint32_t)(g * mma_n), ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+    // ---- TMA producer: warp-uniform loop, lane 0 issues
+    const uint64_t pol = policy_evict_first();  // weights are streamed once
+    int it = 0;                                  // stage counter of this CTA
+    int pre = 0;                                 // stages whose weights went out before griddepcontrol.wait
+    {
+      PieceIter first(g, KB);
+      if (first.next(pc)) {
+        for (int kb = pc.kb0; kb < pc.kb1 && pre < C::NS; kb += KS, ++pre) {
+          const int nk = min(KS, pc.kb1 - kb);
+          if (lane == 0) {
+            mbar_expect_tx(&full[pre], (uint32_t)nk * (C::A_BOX + C::B_BOX));
+            for (int i = 0; i < nk; ++i)
+              tma_load_4d_hint(sA + pre * C::A_BYTES + i * C::A_BOX, &mapW, &full[pre], 0, 0, kb + i, pc.mt, pol);
           }
         }
-        tc_commit(&empty[st]);  // frees the smem stage when these MMAs retire
       }
-      tc_commit(accf);  // accumulator complete
     }
-    __syncwarp();
-  }
-
-  // ---- epilogue: TMEM -> registers -> fp32 partial (all 4 warps)
-  mbar_wait(accf, 0);
-  __syncwarp();
-  tc_fence_after();
-  const int n = m0 + warp * 32 + lane;
-  float* o = out + (size_t)s * (size_t)T * (size_t)N;
-#pragma unroll 1
-  for (int c0 = 0; c0 < TN; c0 += 16) {
-    uint32_t r[16];
-    tc_ld_32x32b_x16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, r);
-    tc_wait_ld();
+    griddep_wait();
+    PieceIter pi(g, KB);
+    while (pi.next(pc)) {
+      for (int kb = pc.kb0; kb < pc.kb1; kb += KS, ++it) {
+        const int st = it % C::NS;
+        const uint32_t ph = (uint32_t)(it / C::NS) & 1u;
+        const int nk = min(KS, pc.kb1 - kb);
+        if (it >= pre) mbar_spin(&empty[st], ph ^ 1u);
+        if (lane == 0) {
+          if (it >= pre) {
+            mbar_expect_tx(&full[st], (uint32_t)nk * (C::A_BOX + C::B_BOX));
+            for (int i = 0; i < nk; ++i)
+              tma_load_4d_hint(sA + st * C::A_BYTES + i * C::A_BOX, &mapW, &full[st], 0, 0, kb + i, pc.mt, pol);
+          }
+          for (int i = 0; i < nk; ++i)
+            tma_load_2d(sB + st * C::B_BYTES + i * C::B_BOX, &mapX, &full[st], (kb + i) * C::BK, pc.tt * TN);
+          if (trace && it < 256) trace[it * 4 + 0] = clock64();
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer: warp-uniform loop, lane 0 issues tcgen05.mma / commit
+    constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MN >> 3) << 17) | ((128u >> 4) << 24);
+    const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
+    const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB));
+    const bool do_mma = !(g.dbg & 1);
+    int it = 0, j = 0;
+    PieceIter pi(g, KB);
+    for (; pi.next(pc); ++j) {
+      const int buf = j & 1;
+      mbar_spin(&tempty[buf], ((uint32_t)(j >> 1) & 1u) ^ 1u);  // epilogue drained this accumulator
+      tc_fence_after();
+      const uint32_t dacc = tmem + (uint32_t)(buf * C::ACC_COLS);
+      for (int kb = pc.kb0; kb < pc.kb1; kb += KS, ++it) {
+        const int st = it % C::NS;
+        const int nk = min(KS, pc.kb1 - kb);
+        mbar_spin(&full[st], (uint32_t)(it / C::NS) & 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          if (trace && it < 256) trace[it * 4 + 1] = clock64();
+          // descriptor of (stage st, box i, k-step kk) = base + byte offset / 16
+          const uint64_t a_st = a_desc0 + (uint64_t)((st * C::A_BYTES) >> 4);
+          const uint64_t b_st = b_desc0 + (uint64_t)((st * C::B_BYTES) >> 4);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int t = t0 + c0 + j;
-      if (t < T) o[(size_t)t * N + n] = __uint_as_float(r[j]);
+          for (int i = 0; i < KS; ++i) {
+            if (i < nk && do_mma) {
+#pragma unroll
+              for (int kk = 0; kk < C::BK / 16; ++kk) {
+                const uint64_t ad = a_st + (uint64_t)((i * C::A_BOX + kk * 32) >> 4);
+#pragma unroll
+                for (int gi = 0; gi < NG; ++gi) {
+                  const uint64_t bd = b_st + (uint64_t)((i * C::B_BOX + gi * MN * 128 + kk * 32) >> 4);
+                  tc_mma_bf16(dacc + (uint32_t)(gi * MN), ad, bd, idesc, (kb + i > pc.kb0 || kk > 0) ? 1u : 0u);
+                }
+              }
+            }
+          }
+          tc_commit(&empty[st]);  // frees the smem stage when these MMAs retire
+          if (trace && it < 256) trace[it * 4 + 2] = clock64();
+        }
+        __syncwarp();
+      }
+      if (lane == 0) tc_commit(&tfull[buf]);  // accumulator complete
+      __syncwarp();
+    }
+  } else {  // ---- epilogue warps 2..5: TMEM lanes 32*(warp%4) ..
+    griddep_wait();
+    const int q = warp & 3;
+    int j = 0;
+    PieceIter pi(g, KB);
+    for (; pi.next(pc); ++j) {
+      const int buf = j & 1;
+      // one thread polls the mbarrier; the other 127 sleep in a named barrier
+      if (warp == 2 && lane == 0) mbar_wait(&tfull[buf], (uint32_t)(j >> 1) & 1u);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      tc_fence_after();
+      const int n = pc.mt * C::BM + q * 32 + lane;
+      float* o = g.out + (size_t)pc.slot * (size_t)g.T * (size_t)g.N;
+      const int t0 = pc.tt * TN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < TN; c0 += 16) {
+        if (t0 + c0 >= g.T) break;
+        uint32_t r[16];
+        tc_ld_32x32b_x16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * C::ACC_COLS + c0), r);
+        tc_wait_ld();
+        if (!(g.dbg & 2)) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int t = t0 + c0 + i;
+            if (t < g.T) o[(size_t)t * g.N + n] = __uint_as_float(r[i]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
     }
   }
+  griddep_launch();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -141,19 +294,22 @@ __global__ void __launch_bounds__(128, 1)
 template <int TT>
 __global__ void __launch_bounds__(256) k_gemm_cc(const uint16_t* __restrict__ x, const uint16_t* __restrict__ W,
                                                  int N, int K, int T, int splits, float* __restrict__ out) {
+  griddep();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = blockIdx.x * 8 + warp;
   const int s = blockIdx.y;
   if (n >= N) return;
   const int KB = K / 64;  // split boundaries on 64-wide blocks, like k_gemm_tc
-  const int k0 = chunk_start(KB, splits, s) * 64, k1 = chunk_start(KB, splits, s + 1) * 64;
+  const int kb0 = chunk_start(KB, splits, s), kb1 = chunk_start(KB, splits, s + 1);
   float acc[TT];
 #pragma unroll
   for (int t = 0; t < TT; ++t) acc[t] = 0.f;
-  const uint16_t* w = W + (size_t)n * K;
+  // tiled weights: row n's 64 elements of k-block kb are 128 contiguous bytes
+  const uint16_t* w = W + tiled_offset((size_t)n, 0, K);
 #pragma unroll 4
-  for (int k = k0 + lane * 8; k < k1; k += 256) {
-    const uint4 wv = __ldg(reinterpret_cast<const uint4*>(w + k));
+  for (int kb = kb0 + (lane >> 3); kb < kb1; kb += 4) {
+    const int k = kb * 64 + (lane & 7) * 8;
+    const uint4 wv = __ldg(reinterpret_cast<const uint4*>(w + (size_t)kb * 8192 + (lane & 7) * 8));
     const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
     for (int t = 0; t < TT; ++t) {
@@ -203,42 +359,87 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, int inner_k, int rows, int b
   return r == CUDA_SUCCESS;
 }
 
-template <int TN>
-static cudaError_t launch_tc_t(const CUtensorMap& mw, const CUtensorMap& mx, int N, int K, int T, int splits,
-                               int mma_n, float* out, cudaStream_t st) {
+// weights in the tiled layout [N/128][K/64][128][64]: 4-D map, box = one
+// contiguous 16 KB tile, coordinates (0, 0, k-block, m-tile)
+bool make_tmap_w_tiled(CUtensorMap* m, const void* base, int K, int N) {
+  if (!get_encode()) return false;
+  const cuuint64_t KB = (cuuint64_t)K / 64;
+  cuuint64_t dims[4] = {64, 128, KB, (cuuint64_t)N / 128};
+  cuuint64_t strides[3] = {128, 128 * 128, 128 * 128 * KB};
+  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || g_num_sms <= 0)
+      g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <int TN, bool MMA16>
+static cudaError_t launch_tc_t(const CUtensorMap& mw, const CUtensorMap& mx, int N, int K, int T, int splits, int G,
+                               float* out, cudaStream_t st) {
   using C = GemmTcCfg<TN>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_gemm_tc<TN, MMA16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(N / 128, (T + TN - 1) / TN, splits);
-  k_gemm_tc<TN><<<grid, 128, C::SMEM, st>>>(mw, mx, N, K, T, splits, mma_n, out);
-  return cudaGetLastError();
+  GemmArgs g;
+  g.N = N; g.K = K; g.T = T; g.splits = G > 0 ? 1 : splits;
+  g.n_m = N / 128; g.n_t = (T + TN - 1) / TN; g.units = g.n_m * g.splits * g.n_t;
+  g.G = G;
+  g.dbg = g_gemm_dbg;
+  g.out = out;
+  const int work = G > 0 ? G * g.n_t : g.units;
+  const int grid = work < num_sms() ? work : num_sms();
+  return launch_k(k_gemm_tc<TN, MMA16>, dim3(grid), dim3(C::THREADS), C::SMEM, st, mw, mx, g);
 }
 
-cudaError_t launch_gemm_tc(const CUtensorMap& mw, const CUtensorMap& mx, int N, int K, int T, int splits,
+template <int TN>
+static cudaError_t launch_tc_m(const CUtensorMap& mw, const CUtensorMap& mx, int N, int K, int T, int splits, int G,
+                               int mma_n, float* out, cudaStream_t st) {
+  if (mma_n == 16 && TN > 16) return launch_tc_t<TN, true>(mw, mx, N, K, T, splits, G, out, st);
+  return launch_tc_t<TN, false>(mw, mx, N, K, T, splits, G, out, st);
+}
+
+cudaError_t launch_gemm_tc(const CUtensorMap& mw, const CUtensorMap& mx, int N, int K, int T, int splits, int G,
                            int tile_n, int mma_n, float* out, cudaStream_t st) {
-  if (mma_n <= 0 || mma_n > tile_n) mma_n = tile_n;
+  if (mma_n != 16) mma_n = tile_n;
   switch (tile_n) {
-    case 16: return launch_tc_t<16>(mw, mx, N, K, T, splits, mma_n, out, st);
-    case 32: return launch_tc_t<32>(mw, mx, N, K, T, splits, mma_n, out, st);
-    case 48: return launch_tc_t<48>(mw, mx, N, K, T, splits, mma_n, out, st);
-    case 64: return launch_tc_t<64>(mw, mx, N, K, T, splits, mma_n, out, st);
-    case 96: return launch_tc_t<96>(mw, mx, N, K, T, splits, mma_n, out, st);
-    case 128: return launch_tc_t<128>(mw, mx, N, K, T, splits, mma_n, out, st);
-    case 256: return launch_tc_t<256>(mw, mx, N, K, T, splits, mma_n, out, st);
+    case 16: return launch_tc_m<16>(mw, mx, N, K, T, splits, G, mma_n, out, st);
+    case 32: return launch_tc_m<32>(mw, mx, N, K, T, splits, G, mma_n, out, st);
+    case 64: return launch_tc_m<64>(mw, mx, N, K, T, splits, G, mma_n, out, st);
+    case 128: return launch_tc_m<128>(mw, mx, N, K, T, splits, G, mma_n, out, st);
+    case 256: return launch_tc_m<256>(mw, mx, N, K, T, splits, G, mma_n, out, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+int part_slots(const PartSpec& p, int N) {
+  int mx = 1;
+  for (int n = 0; n < N; n += 128) {
+    const int c = part_count(p, n);
+    mx = c > mx ? c : mx;
+  }
+  return mx;
 }
 
 int gemm_tile_n(int T) {
   if (T <= 16) return 16;
   if (T <= 32) return 32;
-  if (T <= 48) return 48;
   if (T <= 64) return 64;
-  if (T <= 96) return 96;
   if (T <= 128) return 128;
   return 256;
 }
@@ -247,13 +448,12 @@ cudaError_t launch_gemm_cc(const uint16_t* x, const uint16_t* W, int N, int K, i
                            cudaStream_t st) {
   dim3 grid((N + 7) / 8, splits);
   switch (T) {
-    case 1: k_gemm_cc<1><<<grid, 256, 0, st>>>(x, W, N, K, T, splits, out); break;
-    case 2: k_gemm_cc<2><<<grid, 256, 0, st>>>(x, W, N, K, T, splits, out); break;
-    case 3: case 4: k_gemm_cc<4><<<grid, 256, 0, st>>>(x, W, N, K, T, splits, out); break;
-    case 5: case 6: case 7: case 8: k_gemm_cc<8><<<grid, 256, 0, st>>>(x, W, N, K, T, splits, out); break;
+    case 1: return launch_k(k_gemm_cc<1>, grid, dim3(256), 0, st, x, W, N, K, T, splits, out);
+    case 2: return launch_k(k_gemm_cc<2>, grid, dim3(256), 0, st, x, W, N, K, T, splits, out);
+    case 3: case 4: return launch_k(k_gemm_cc<4>, grid, dim3(256), 0, st, x, W, N, K, T, splits, out);
+    case 5: case 6: case 7: case 8: return launch_k(k_gemm_cc<8>, grid, dim3(256), 0, st, x, W, N, K, T, splits, out);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace mg

@@ -7,7 +7,31 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
+#include "common.cuh"
+
 namespace mg {
+
+// ---- launch helper: programmatic dependent launch (PDL) on every kernel of
+// the decode path, so a kernel's prologue (barrier init, TMEM alloc, weight
+// prefetch) overlaps the tail of its predecessor.
+extern int g_pdl;  // 1 = launch with programmatic stream serialization
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 // ---- weights (K0)
 struct GenSpec {
@@ -16,15 +40,31 @@ struct GenSpec {
   int64_t n;        // logical elements
   int32_t kind;     // 0 proj, 1 embed, 2 gain, 3 bias
   int32_t fan_in;
-  int32_t row_len;  // logical row length (for remaps)
+  int32_t row_len;  // logical row length K (for remaps / tiling)
   int32_t remap;    // 0 identity, 1 gate rows of the 64-interleaved [gate;up], 2 up rows
+  int32_t row_off;  // physical row of logical row 0 (q|k|v inside the fused QKV matrix)
+  int32_t tiled;    // 1: GEMM weight layout [N/128][K/64][128][64] (see tiled_offset)
 };
+// Physical offset of element (row, col) of a weight matrix with K columns in
+// the tiled layout: 128 x 64 tiles, k-blocks of one 128-row tile contiguous,
+// so every TMA box (and every stream-K range) is one contiguous HBM stream.
+__host__ __device__ __forceinline__ size_t tiled_offset(size_t row, size_t col, int K) {
+  const size_t KB = (size_t)K / 64;
+  return (((row / 128) * KB + col / 64) * 128 + row % 128) * 64 + col % 64;
+}
+bool make_tmap_w_tiled(CUtensorMap* m, const void* base, int K, int N);
 cudaError_t launch_gen(const GenSpec& g, uint16_t* dst, cudaStream_t st);
 
 // ---- GEMM (a3, a5-a8)
 bool make_tmap_2d(CUtensorMap* m, const void* base, int inner_k, int rows, int box_rows);
-cudaError_t launch_gemm_tc(const CUtensorMap& mw, const CUtensorMap& mx, int N, int K, int T, int splits,
+// splits: uniform split-K (G == 0) or ignored; G > 0: stream-K over G
+// virtual CTAs per token tile (partial slots per tile: part_count()).
+// tile_n in {16, 32, 64, 128, 256}; mma_n 16 (verifier slot groups) or tile_n
+cudaError_t launch_gemm_tc(const CUtensorMap& mw, const CUtensorMap& mx, int N, int K, int T, int splits, int G,
                            int tile_n, int mma_n, float* out, cudaStream_t st);
+// max partial slots of any tile for a GEMM shape (buffer sizing)
+int part_slots(const PartSpec& p, int N);
+int num_sms();
 cudaError_t launch_gemm_cc(const uint16_t* x, const uint16_t* W, int N, int K, int T, int splits, float* out,
                            cudaStream_t st);
 int gemm_tile_n(int T);
@@ -47,13 +87,17 @@ cudaError_t launch_rmsnorm(const uint16_t* x, const uint16_t* w, int T, int d, f
                            cudaStream_t st);
 // qkv: part[S][T][NQKV] -> q[T][H*hd]; k, v appended to the cache at (slot, pos)
 // (cache == nullptr: dense k_out/v_out [T][KV*hd] instead)
-cudaError_t launch_epi_qkv(const float* part, int S, const uint16_t* bias, const int32_t* pos, int T, int H, int KV,
-                           int hd, const float* rope_cos, const float* rope_sin, uint16_t* q,
+cudaError_t launch_epi_qkv(const float* part, PartSpec ps, const uint16_t* bias, const int32_t* pos, int T, int H,
+                           int KV, int hd, const float* rope_cos, const float* rope_sin, uint16_t* q,
                            const CacheView* cache, const int32_t* slot, uint16_t* k_out, uint16_t* v_out,
                            cudaStream_t st);
-cudaError_t launch_epi_residual(const uint16_t* x, const float* part, int S, int T, int N, uint16_t* out,
+cudaError_t launch_epi_residual(const uint16_t* x, const float* part, PartSpec ps, int T, int N, uint16_t* out,
                                 cudaStream_t st);
-cudaError_t launch_epi_swiglu(const float* part, int S, int T, int F, uint16_t* out, cudaStream_t st);
+// x <- bf16(x + sum_s part[s]); xn <- RMSNorm(x, w) (xn nullable)
+cudaError_t launch_residual_norm(uint16_t* x, const float* part, PartSpec ps, int T, int d, const uint16_t* w,
+                                 float eps, uint16_t* xn, cudaStream_t st);
+int attn_max_chunk();
+cudaError_t launch_epi_swiglu(const float* part, PartSpec ps, int T, int F, uint16_t* out, cudaStream_t st);
 cudaError_t launch_gather_rows(const uint16_t* src, const int32_t* rows, int n, int d, uint16_t* dst,
                                cudaStream_t st);
 

@@ -57,14 +57,24 @@ def rmsnorm(x: np.ndarray, w: np.ndarray, eps: float) -> np.ndarray:
     return to_host_u16(out)
 
 
+def streamk_counts(N: int, K: int, G: int) -> list[int]:
+    """Pieces per 128-feature tile of the stream-K partition (include/mg_debug.h)."""
+    KB, n_m = K // 64, N // 128
+    W = n_m * KB
+    owner = lambda w: ((w + 1) * G - 1) // W
+    return [owner((m + 1) * KB - 1) - owner(m * KB) + 1 for m in range(n_m)]
+
+
 def gemm(x: np.ndarray, W: np.ndarray, splits=1, impl=0, mma_n=0, tile_n=0, x_dev=None, w_dev=None):
-    """Returns the per-split fp32 partials [splits, T, N]."""
+    """Returns the fp32 partials [slots, T, N] (splits < 0: stream-K pieces,
+    tile m's pieces in slots 0..streamk_counts()[m]-1, k order)."""
     torch = _t()
     T, K = x.shape
     N = W.shape[0]
     xd = x_dev if x_dev is not None else to_dev_u16(x)
     wd = w_dev if w_dev is not None else to_dev_u16(W)
-    out = torch.full((splits, T, N), float("nan"), dtype=torch.float32, device="cuda")
+    slots = splits if splits > 0 else max(streamk_counts(N, K, -splits))
+    out = torch.full((slots, T, N), float("nan"), dtype=torch.float32, device="cuda")
     check(lib().mgd_gemm(_p(xd), _p(wd), T, N, K, splits, impl, mma_n, tile_n, _p(out), _stream()), None, "gemm")
     _sync()
     return out.cpu().numpy()

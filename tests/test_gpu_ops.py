@@ -54,11 +54,23 @@ def test_rmsnorm(orc, K, T, d):
 
 
 # ------------------------------------------------------------------ GEMM
-def _check_gemm(orc, x, W, part):
-    xf, Wf = _bf(orc, x), _bf(orc, W)
-    y = part[0].astype(np.float32)
+def _sum_pieces(part, counts=None):
+    """Sum the fp32 partial slots in k order (per 128-feature tile for stream-K)."""
+    y = part[0].astype(np.float32).copy()
     for s in range(1, part.shape[0]):
-        y = (y + part[s]).astype(np.float32)
+        if counts is None:
+            y = (y + part[s]).astype(np.float32)
+        else:
+            for m, c in enumerate(counts):
+                if s < c:
+                    sl = slice(128 * m, 128 * (m + 1))
+                    y[:, sl] = (y[:, sl] + part[s][:, sl]).astype(np.float32)
+    return y
+
+
+def _check_gemm(orc, x, W, part, counts=None):
+    xf, Wf = _bf(orc, x), _bf(orc, W)
+    y = _sum_pieces(part, counts)
     ref = orc.gemm(x, W, 1).astype(np.float64)
     scale = np.abs(xf) @ np.abs(Wf).T
     err = np.abs(y - ref)
@@ -68,8 +80,8 @@ def _check_gemm(orc, x, W, part):
 
 @pytest.mark.parametrize("T,N,K_,splits,mma_n,tile_n", [
     (1, 128, 64, 1, 0, 16), (5, 256, 256, 1, 0, 16), (16, 384, 512, 2, 16, 16), (17, 256, 256, 1, 0, 32),
-    (48, 128, 1024, 3, 16, 48), (64, 512, 4096, 7, 0, 64), (64, 512, 4096, 7, 16, 64), (100, 256, 768, 1, 16, 128),
-    (256, 128, 256, 1, 0, 256), (300, 256, 512, 2, 16, 256), (96, 128, 14336, 16, 32, 96)])
+    (48, 128, 1024, 3, 16, 64), (64, 512, 4096, 7, 0, 64), (64, 512, 4096, 7, 16, 64), (100, 256, 768, 1, 16, 128),
+    (256, 128, 256, 1, 0, 256), (300, 256, 512, 2, 16, 256), (96, 128, 14336, 16, 0, 128), (3, 128, 192, 3, 0, 16)])
 def test_gemm_tcgen05(orc, K, T, N, K_, splits, mma_n, tile_n):
     rng = np.random.default_rng(T * 131 + N + K_)
     x = _rand(orc, rng, (T, K_))
@@ -85,6 +97,36 @@ def test_gemm_tcgen05(orc, K, T, N, K_, splits, mma_n, tile_n):
         sub = orc.gemm(np.ascontiguousarray(x[:, lo:hi]), np.ascontiguousarray(W[:, lo:hi]), 1)
         sc = np.abs(_bf(orc, x[:, lo:hi])) @ np.abs(_bf(orc, W[:, lo:hi])).T
         assert np.all(np.abs(part[s] - sub) <= 1e-5 * sc + 1e-30)
+
+
+@pytest.mark.parametrize("T,N,K_,G,mma_n,tile_n", [
+    (1, 128, 256, 3, 16, 16), (16, 6144, 4096, 148, 16, 16), (64, 4096, 4096, 148, 0, 64),
+    (64, 4096, 14336, 148, 16, 64), (33, 1024, 1024, 7, 16, 64), (300, 768, 256, 5, 16, 256),
+    (8, 28672 // 8, 4096, 148, 0, 16), (128, 1024, 640, 29, 0, 128)])
+def test_gemm_tcgen05_streamk(orc, K, T, N, K_, G, mma_n, tile_n):
+    """Stream-K partition (the engine's schedule): tile m's pieces, summed in
+    k order, equal the full dot product within the fp32 tolerance; every
+    piece is the dot product over exactly its k-block range."""
+    rng = np.random.default_rng(T + N + G)
+    x = _rand(orc, rng, (T, K_))
+    W = _rand(orc, rng, (N, K_), 1 / np.sqrt(K_))
+    part = K.gemm(x, W, splits=-G, impl=0, mma_n=mma_n, tile_n=tile_n)
+    counts = K.streamk_counts(N, K_, G)
+    _check_gemm(orc, x, W, part, counts)
+    KB, n_m = K_ // 64, N // 128
+    Wk = n_m * KB
+    for m in (0, n_m // 2, n_m - 1):
+        w0 = m * KB
+        first = ((w0 + 1) * G - 1) // Wk
+        for p in range(counts[m]):
+            i = first + p
+            lo = max(i * Wk // G, w0) - w0
+            hi = min((i + 1) * Wk // G, w0 + KB) - w0
+            sl = slice(128 * m, 128 * (m + 1))
+            sub = orc.gemm(np.ascontiguousarray(x[:, 64 * lo:64 * hi]),
+                           np.ascontiguousarray(W[sl, 64 * lo:64 * hi]), 1)
+            sc = np.abs(_bf(orc, x[:, 64 * lo:64 * hi])) @ np.abs(_bf(orc, W[sl, 64 * lo:64 * hi])).T
+            assert np.all(np.abs(part[p][:, sl] - sub) <= 1e-5 * sc + 1e-30), (m, p)
 
 
 @pytest.mark.parametrize("T", [1, 2, 3, 4, 8])
@@ -104,15 +146,17 @@ def test_gemm_column_invariance(orc, K):
     N, K_ = 256, 2048
     W = _rand(orc, rng, (N, K_), 1 / np.sqrt(K_))
     target = _rand(orc, rng, (1, K_))
-    ref = K.gemm(target, W, splits=4, impl=0, mma_n=16, tile_n=16)[:, 0]
-    for T in (2, 15, 16, 33, 64, 130, 256):
-        others = _rand(orc, rng, (T, K_), 3.0)
-        for col in sorted(c for c in {0, 1, 15, T // 2, T - 1} if c < T):
-            x = others.copy()
-            x[col] = target[0]
-            for tile in sorted({16, 64, 256} | {t for t in (32, 48, 96, 128) if t >= 16}):
-                part = K.gemm(x, W, splits=4, impl=0, mma_n=16, tile_n=tile)
-                assert np.array_equal(part[:, col], ref), (T, col, tile)
+    for splits in (4, -5):  # uniform split-K and the engine's stream-K partition
+        ref = K.gemm(target, W, splits=splits, impl=0, mma_n=16, tile_n=16)[:, 0]
+        for T in (2, 15, 16, 33, 64, 130, 256, 300):
+            others = _rand(orc, rng, (T, K_), 3.0)
+            for col in sorted(c for c in {0, 1, 15, T // 2, T - 1} if c < T):
+                x = others.copy()
+                x[col] = target[0]
+                for tile in (16, 32, 64, 128, 256):
+                    part = K.gemm(x, W, splits=splits, impl=0, mma_n=16, tile_n=tile)
+                    ok = np.isnan(ref) == np.isnan(part[:, col])
+                    assert ok.all() and np.array_equal(np.nan_to_num(part[:, col]), np.nan_to_num(ref)), (T, col, tile)
 
 
 # ------------------------------------------------------------------ a3 epilogue
@@ -134,8 +178,8 @@ def test_qkv_epilogue_bit_exact(orc, K, H, KV, hd, bias, S):
 
 
 # ------------------------------------------------------------------ a4
-@pytest.mark.parametrize("H,KV,hd,chunk", [(4, 4, 64, 16), (32, 8, 128, 256), (40, 8, 128, 64),
-                                           (28, 4, 128, 512), (32, 8, 128, 100)])
+@pytest.mark.parametrize("H,KV,hd,chunk", [(4, 4, 64, 64), (4, 2, 64, 128), (32, 8, 128, 256), (40, 8, 128, 64),
+                                           (28, 4, 128, 128), (32, 8, 128, 64), (64, 4, 128, 128)])
 def test_attention(orc, K, H, KV, hd, chunk):
     rng = np.random.default_rng(H * hd + chunk)
     T, stride = 4, 700
