@@ -173,56 +173,48 @@ __global__ void __launch_bounds__(kAtThreads) k_attn_chunk(AttnArgs a) {
   }
   __syncthreads();
 
-  // ---- softmax over the chunk, per query head (fixed trees; rows >= G zeroed)
-  const int nk16 = nblk * 16;
-  for (int g = 0; g < 16; ++g) {
-    if (g >= G) {
-      for (int j = threadIdx.x; j < nk16; j += kAtThreads) S[g * C::CH + j] = 0.f;
-      continue;
-    }
+  // ---- softmax over the chunk: query head g is owned by warp g % 4, lane l
+  // takes keys l, l+32, ... (fixed trees, no CTA-wide barrier per head)
+  for (int g = warp; g < G; g += 4) {
+    float* sg = S + g * C::CH;
     float m = -INFINITY;
-    for (int j = threadIdx.x; j < len; j += kAtThreads) m = fmaxf(m, S[g * C::CH + j]);
+    for (int j = lane; j < len; j += 32) m = fmaxf(m, sg[j]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if (lane == 0) red[warp * 16 + g] = m;
-  }
-  __syncthreads();
-  if (threadIdx.x < G) {
-    const int g = threadIdx.x;
-    s_ml[g] = fmaxf(fmaxf(red[g], red[16 + g]), fmaxf(red[32 + g], red[48 + g]));
-  }
-  __syncthreads();
-  for (int g = 0; g < G; ++g) {
-    const float m = s_ml[g];
     float l = 0.f;
-    for (int j = threadIdx.x; j < nk16; j += kAtThreads) {
-      const float e = j < len ? expf(__fsub_rn(S[g * C::CH + j], m)) : 0.f;
-      S[g * C::CH + j] = e;
+    for (int j = lane; j < C::CH; j += 32) {
+      const float e = j < len ? expf(__fsub_rn(sg[j], m)) : 0.f;
+      sg[j] = e;
       l = __fadd_rn(l, e);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) l = __fadd_rn(l, __shfl_xor_sync(0xffffffffu, l, off));
-    if (lane == 0) red[warp * 16 + g] = l;
+    if (lane == 0) {
+      s_ml[g] = m;
+      s_ml[16 + g] = l;
+    }
   }
   __syncthreads();
-  if (threadIdx.x < G) {
-    const int g = threadIdx.x;
-    s_ml[16 + g] = __fadd_rn(__fadd_rn(red[g], red[16 + g]), __fadd_rn(red[32 + g], red[48 + g]));
-  }
 
-  // ---- pass 2: acc = sum_j e_j v_j  (e = hi + lo, two bf16 MMAs)
-  float acc[HD / 8][4];
+  // ---- pass 2: acc = sum_j e_j v_j  (e = hi + lo, two bf16 MMAs).  Warp w owns
+  // head dims [w*HD/4, (w+1)*HD/4) and sums ALL the chunk's key blocks in order,
+  // so no cross-warp reduction is needed.
+  constexpr int NT = HD / 32;  // 8-dim n-tiles per warp
+  float acc[NT][4];
 #pragma unroll
-  for (int nt = 0; nt < HD / 8; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
-  mbar_wait(&bars[4 + warp], 0);
-  for (int j = 0; j < nbw; ++j) {
-    const uint32_t vb = smem_u32(kvr + ((size_t)(4 + warp) * NB + j) * C::BLKB);
-    const int j0 = 16 * (warp + 4 * j);
+  for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+  for (int w = 0; w < 4; ++w) mbar_wait(&bars[4 + w], 0);  // every warp's V rows landed
+  const int d0 = warp * (HD / 4);
+  for (int b = 0; b < nblk; ++b) {
+    const uint32_t vb = smem_u32(kvr + ((size_t)(4 + (b & 3)) * NB + (b >> 2)) * C::BLKB);
+    const int j0 = 16 * b;
     uint32_t ph[4], pl[4];
     {
       const float* s0 = S + r0 * C::CH + j0 + cc;
       const float* s1 = S + r1 * C::CH + j0 + cc;
-      const float e[8] = {s0[0], s0[1], s1[0], s1[1], s0[8], s0[9], s1[8], s1[9]};
+      const bool g0 = r0 < G, g1 = r1 < G;  // rows >= G are padding: P = 0
+      const float e[8] = {g0 ? s0[0] : 0.f, g0 ? s0[1] : 0.f, g1 ? s1[0] : 0.f, g1 ? s1[1] : 0.f,
+                          g0 ? s0[8] : 0.f, g0 ? s0[9] : 0.f, g1 ? s1[8] : 0.f, g1 ? s1[9] : 0.f};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const uint32_t h = pack_bf2(e[2 * q], e[2 * q + 1]);
@@ -231,40 +223,33 @@ __global__ void __launch_bounds__(kAtThreads) k_attn_chunk(AttnArgs a) {
       }
     }
 #pragma unroll
-    for (int n2 = 0; n2 < HD / 16; ++n2) {
+    for (int n2 = 0; n2 < NT / 2; ++n2) {
       uint32_t b0, b1, b2, b3;
       const int mi = lane >> 3, rr = lane & 7;
-      ldsm_x4_t(vb + ((mi & 1) * 8 + rr) * C::ROWB + (16 * n2 + 8 * (mi >> 1)) * 2, b0, b1, b2, b3);
+      ldsm_x4_t(vb + ((mi & 1) * 8 + rr) * C::ROWB + (d0 + 16 * n2 + 8 * (mi >> 1)) * 2, b0, b1, b2, b3);
       mma_bf16(acc[2 * n2], ph, b0, b1);
       mma_bf16(acc[2 * n2], pl, b0, b1);
       mma_bf16(acc[2 * n2 + 1], ph, b2, b3);
       mma_bf16(acc[2 * n2 + 1], pl, b2, b3);
     }
   }
-  __syncthreads();
-  // ---- add the 4 warps' partial sums in warp order (scratch aliases the K/V blocks)
-  float* X = reinterpret_cast<float*>(kvr);  // [4][16][HD]
+  // ---- write the chunk partials (rows < G)
 #pragma unroll
-  for (int nt = 0; nt < HD / 8; ++nt) {
-    float* xw = X + (size_t)warp * 16 * HD;
-    xw[r0 * HD + 8 * nt + cc] = acc[nt][0];
-    xw[r0 * HD + 8 * nt + cc + 1] = acc[nt][1];
-    xw[r1 * HD + 8 * nt + cc] = acc[nt][2];
-    xw[r1 * HD + 8 * nt + cc + 1] = acc[nt][3];
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < G * HD; e += kAtThreads) {
-    const int g = e / HD, d = e % HD;
-    float v = X[g * HD + d];
-    v = __fadd_rn(v, X[16 * HD + g * HD + d]);
-    v = __fadd_rn(v, X[32 * HD + g * HD + d]);
-    v = __fadd_rn(v, X[48 * HD + g * HD + d]);
-    const size_t o = po + (size_t)g * a.n_chunks;
-    a.part_acc[o * HD + d] = v;
-    if (d == 0) {
-      a.part_ml[o * 2 + 0] = s_ml[g];
-      a.part_ml[o * 2 + 1] = s_ml[16 + g];
+  for (int nt = 0; nt < NT; ++nt) {
+    const int d = d0 + 8 * nt + cc;
+    if (r0 < G) {
+      float* o = a.part_acc + (po + (size_t)r0 * a.n_chunks) * HD + d;
+      *reinterpret_cast<float2*>(o) = make_float2(acc[nt][0], acc[nt][1]);
     }
+    if (r1 < G) {
+      float* o = a.part_acc + (po + (size_t)r1 * a.n_chunks) * HD + d;
+      *reinterpret_cast<float2*>(o) = make_float2(acc[nt][2], acc[nt][3]);
+    }
+  }
+  if (threadIdx.x < G) {
+    const size_t o = po + (size_t)threadIdx.x * a.n_chunks;
+    a.part_ml[o * 2 + 0] = s_ml[threadIdx.x];
+    a.part_ml[o * 2 + 1] = s_ml[16 + threadIdx.x];
   }
 }
 

@@ -80,7 +80,7 @@ __device__ __forceinline__ float block_inv_rms(float ss, int d, float eps, float
   __syncthreads();
   if (threadIdx.x == 0) {
     float s = red[0];
-    for (int i = 1; i < 8; ++i) s = __fadd_rn(s, red[i]);
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) s = __fadd_rn(s, red[i]);
     const float mean = __fdiv_rn(s, (float)d);
     *s_inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(mean, eps)));
   }
@@ -133,16 +133,55 @@ cudaError_t launch_rmsnorm(const uint16_t* x, const uint16_t* w, int T, int d, f
 // ------------------------------------------------------------------ a5/a7 (+a2): residual + RMSNorm
 // x <- bf16(x + sum_s part[s]) (splits summed in order), then xn <- RMSNorm(x)
 // with the same fixed tree as k_rmsnorm.  One CTA per token.
+// sum of the S partial slots of one output, in slot (= k) order; the first 8
+// loads are issued together (predicated), the adds stay in order
 __device__ __forceinline__ float sum_splits(const float* __restrict__ part, int S, size_t stride, size_t idx) {
-  float a = part[idx];
-  for (int s = 1; s < S; ++s) a = __fadd_rn(a, part[(size_t)s * stride + idx]);
+  float v[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v[s] = s < S ? part[(size_t)s * stride + idx] : 0.f;
+  float a = v[0];
+#pragma unroll
+  for (int s = 1; s < 8; ++s)
+    if (s < S) a = __fadd_rn(a, v[s]);
+  for (int s = 8; s < S; ++s) a = __fadd_rn(a, part[(size_t)s * stride + idx]);
   return a;
 }
 
-__global__ void __launch_bounds__(256) k_residual_norm(uint16_t* __restrict__ x, const float* __restrict__ part,
-                                                       PartSpec ps, int T, int d, const uint16_t* __restrict__ w,
-                                                       float eps, uint16_t* __restrict__ xn) {
-  __shared__ float red[8];
+// 8 consecutive fp32 partial sums (one 8-feature vector), pieces added in order;
+// the loads of up to 8 pieces are issued together
+__device__ __forceinline__ void sum8_pieces(const float* __restrict__ part, int S, size_t stride, size_t idx,
+                                            float* out) {
+  float4 lo[8], hi[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    if (s < S) {
+      lo[s] = *reinterpret_cast<const float4*>(part + (size_t)s * stride + idx);
+      hi[s] = *reinterpret_cast<const float4*>(part + (size_t)s * stride + idx + 4);
+    }
+  }
+  float a[8] = {lo[0].x, lo[0].y, lo[0].z, lo[0].w, hi[0].x, hi[0].y, hi[0].z, hi[0].w};
+#pragma unroll
+  for (int s = 1; s < 8; ++s) {
+    if (s < S) {
+      a[0] = __fadd_rn(a[0], lo[s].x); a[1] = __fadd_rn(a[1], lo[s].y);
+      a[2] = __fadd_rn(a[2], lo[s].z); a[3] = __fadd_rn(a[3], lo[s].w);
+      a[4] = __fadd_rn(a[4], hi[s].x); a[5] = __fadd_rn(a[5], hi[s].y);
+      a[6] = __fadd_rn(a[6], hi[s].z); a[7] = __fadd_rn(a[7], hi[s].w);
+    }
+  }
+  for (int s = 8; s < S; ++s)
+    for (int k = 0; k < 8; ++k) a[k] = __fadd_rn(a[k], part[(size_t)s * stride + idx + k]);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) out[k] = a[k];
+}
+
+constexpr int kResThreads = 512;
+
+__global__ void __launch_bounds__(kResThreads) k_residual_norm(uint16_t* __restrict__ x, const float* __restrict__ part,
+                                                               PartSpec ps, int T, int d,
+                                                               const uint16_t* __restrict__ w, float eps,
+                                                               uint16_t* __restrict__ xn) {
+  __shared__ float red[kResThreads / 32];
   __shared__ float s_inv;
   extern __shared__ uint4 hrow[];  // the new residual row, d/8 vectors
   griddep();
@@ -151,18 +190,15 @@ __global__ void __launch_bounds__(256) k_residual_norm(uint16_t* __restrict__ x,
   uint4* xv = reinterpret_cast<uint4*>(x + (size_t)t * d);
   const int nv = d / 8;
   float ss = 0.f;
-  for (int i = threadIdx.x; i < nv; i += 256) {
+  for (int i = threadIdx.x; i < nv; i += kResThreads) {
     const uint4 v = xv[i];
     const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+    float acc[8];
+    sum8_pieces(part, part_count(ps, i * 8), stride, (size_t)t * d + (size_t)i * 8, acc);  // one 128-feature tile
     uint32_t r[4];
-    const size_t base = (size_t)t * d + (size_t)i * 8;
-    const int S = part_count(ps, i * 8);  // the 8 features share one 128-feature tile
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float a = __fadd_rn(lo_bf(u[j]), sum_splits(part, S, stride, base + 2 * j));
-      const float b = __fadd_rn(hi_bf(u[j]), sum_splits(part, S, stride, base + 2 * j + 1));
-      r[j] = pack_bf2(a, b);
-    }
+    for (int j = 0; j < 4; ++j)
+      r[j] = pack_bf2(__fadd_rn(lo_bf(u[j]), acc[2 * j]), __fadd_rn(hi_bf(u[j]), acc[2 * j + 1]));
     const uint4 h = make_uint4(r[0], r[1], r[2], r[3]);
     hrow[i] = h;
     xv[i] = h;
@@ -172,12 +208,12 @@ __global__ void __launch_bounds__(256) k_residual_norm(uint16_t* __restrict__ x,
   if (!xn) return;
   const uint4* wv = reinterpret_cast<const uint4*>(w);
   uint4* ov = reinterpret_cast<uint4*>(xn + (size_t)t * d);
-  for (int i = threadIdx.x; i < nv; i += 256) ov[i] = norm8(hrow[i], __ldg(wv + i), inv);
+  for (int i = threadIdx.x; i < nv; i += kResThreads) ov[i] = norm8(hrow[i], __ldg(wv + i), inv);
 }
 
 cudaError_t launch_residual_norm(uint16_t* x, const float* part, PartSpec ps, int T, int d, const uint16_t* w,
                                  float eps, uint16_t* xn, cudaStream_t st) {
-  return launch_k(k_residual_norm, dim3(T), dim3(256), (size_t)d * 2, st, x, part, ps, T, d, w, eps, xn);
+  return launch_k(k_residual_norm, dim3(T), dim3(kResThreads), (size_t)d * 2, st, x, part, ps, T, d, w, eps, xn);
 }
 
 // ------------------------------------------------------------------ a3 epilogue

@@ -424,23 +424,63 @@ static mg_status apply_pt(mg_ctx* c, const std::vector<std::pair<int, int>>& upd
 // (cu_* arrays, entries [0, M)), in chunks of Tv tokens, then the LM head +
 // top-2 on the rows' last tokens `last_host` (list indices, ascending),
 // writing v arrays [0, n_last).
+// Run `body` (a pure launch sequence on c->st with fixed pointers) through a
+// CUDA graph keyed by `key`: eager on first use, captured and instantiated on
+// the second, replayed afterwards (PDL edges are kept as programmatic edges).
+template <class F>
+static mg_status graphed(mg_ctx* c, const std::tuple<int, int, int, int, int, int>& key, F&& body) {
+  if (!c->use_graphs || c->timing.on || c->capture) return body();
+  auto& g = c->graphs[key];
+  if (g.exec) {
+    CK(cudaGraphLaunch(g.exec, c->st));
+    c->launches += g.launches;
+    return MG_OK;
+  }
+  if (++g.seen < 2) return body();
+  // capture on a private stream (the caller's may be the legacy default stream,
+  // which cannot be captured); the instantiated graph is launched on c->st
+  if (!c->cap_st) CK(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking));
+  const unsigned long long l0 = c->launches;
+  cudaStream_t user = c->st;
+  CK(cudaStreamBeginCapture(c->cap_st, cudaStreamCaptureModeThreadLocal));
+  c->st = c->cap_st;
+  mg_status r = body();
+  c->st = user;
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->cap_st, &graph);
+  if (r) {
+    if (graph) cudaGraphDestroy(graph);
+    return r;
+  }
+  CK(e);
+  e = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  CK(e);
+  g.launches = c->launches - l0;
+  CK(cudaGraphLaunch(g.exec, c->st));
+  return MG_OK;
+}
+
 static mg_status run_det(mg_ctx* c, int M, const std::vector<int>& last_host, int max_ctx_hint) {
   int r0 = 0;  // next gated row whose last token is pending
   const int n_last = (int)last_host.size();
   for (int c0 = 0; c0 < M; c0 += c->Tv) {
     const int T = M - c0 < c->Tv ? M - c0 : c->Tv;
     Sched sc = sched_det(c, T, max_ctx_hint);
-    mg_status r = forward(c, T, c->cu_slot + c0, c->cu_pos + c0, c->cu_tok + c0, c->cu_nk + c0, 1, sc);
-    if (r) return r;
     int r1 = r0;
     while (r1 < n_last && last_host[r1] < c0 + T) ++r1;
-    if (r1 > r0) {
-      CK(launch_gather_rows_sub(c->xn, c->last_d + r0, c0, r1 - r0, c->d, c->xgn, c->st));
-      c->launches++;
-      if ((r = lm_head(c, c->xgn, c->cfg.max_batch, r1 - r0, sc.lm, c->v_v1 + r0, c->v_tok + r0,
-                       c->v_v2 + r0, c->v_i2 + r0, c->v_g + r0)))
-        return r;
-    }
+    mg_status r = graphed(c, std::make_tuple(1, T, sc.attn_nch, c0, r0, r1), [&]() -> mg_status {
+      mg_status rr = forward(c, T, c->cu_slot + c0, c->cu_pos + c0, c->cu_tok + c0, c->cu_nk + c0, 1, sc);
+      if (rr) return rr;
+      if (r1 > r0) {
+        CK(launch_gather_rows_sub(c->xn, c->last_d + r0, c0, r1 - r0, c->d, c->xgn, c->st));
+        c->launches++;
+        return lm_head(c, c->xgn, c->cfg.max_batch, r1 - r0, sc.lm, c->v_v1 + r0, c->v_tok + r0, c->v_v2 + r0,
+                       c->v_i2 + r0, c->v_g + r0);
+      }
+      return MG_OK;
+    });
+    if (r) return r;
     r0 = r1;
   }
   return MG_OK;
@@ -667,14 +707,17 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
       c->launches++;
     }
   }
-  // 2. fast path
-  CK(launch_prepare(c->slots_d, B, c->pos_d, c->hist_d, c->cfg.max_seq + 1, c->f_slot, c->f_pos, c->f_tok, c->f_nk,
-                    c->st));
-  c->launches++;
+  // 2. fast path (one CUDA graph per (B, attention chunks))
   Sched fs = sched_fast(c, B, max_ctx);
-  mg_status r = forward(c, B, c->f_slot, c->f_pos, c->f_tok, c->f_nk, 0, fs);
+  mg_status r = graphed(c, std::make_tuple(0, B, fs.attn_nch, 0, 0, 0), [&]() -> mg_status {
+    CK(launch_prepare(c->slots_d, B, c->pos_d, c->hist_d, c->cfg.max_seq + 1, c->f_slot, c->f_pos, c->f_tok,
+                      c->f_nk, c->st));
+    c->launches++;
+    mg_status rr = forward(c, B, c->f_slot, c->f_pos, c->f_tok, c->f_nk, 0, fs);
+    if (rr) return rr;
+    return lm_head(c, c->xn, c->Tmax, B, fs.lm, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g);
+  });
   if (r) return r;
-  if ((r = lm_head(c, c->xn, c->Tmax, B, fs.lm, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g))) return r;
   if (c->capture) CK(cudaMemcpyAsync(c->capture, c->logits, (size_t)B * c->V * 4, cudaMemcpyDeviceToDevice, c->st));
 
   // 3. gate (+ 4. verifier)
@@ -765,6 +808,9 @@ void mg_destroy(mg_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->st);
   for (auto e : c->timing.pool) cudaEventDestroy(e);
+  for (auto& kv : c->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  if (c->cap_st) cudaStreamDestroy(c->cap_st);
   if (c->stage_ev[0]) cudaEventDestroy(c->stage_ev[0]);
   if (c->stage_ev[1]) cudaEventDestroy(c->stage_ev[1]);
   if (c->pinned) cudaFreeHost(c->pinned);

@@ -112,4 +112,15 @@ struct mg_ctx {
   std::map<std::tuple<const void*, int, int, int>, CUtensorMap> xmaps;
   unsigned long long launches = 0;
   mg::Timing timing;
+
+  // CUDA graphs of the launch sequences (fast step per (B, attention chunks);
+  // verifier chunks per (T, chunks, offsets)); captured on the second use
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    int seen = 0;
+    unsigned long long launches = 0;
+  };
+  std::map<std::tuple<int, int, int, int, int, int>, GraphEntry> graphs;
+  bool use_graphs = true;
+  cudaStream_t cap_st = nullptr;  // private capture stream
 };
