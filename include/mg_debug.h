@@ -46,11 +46,14 @@ mg_status mgd_qkv_epilogue(const float* part, int32_t splits, const uint16_t* bi
                            int32_t T, int32_t H, int32_t KV, int32_t hd, float theta, int32_t max_pos,
                            uint16_t* q, uint16_t* k, uint16_t* v, void* stream);
 
-/* Decode attention over a dense per-token K/V:
- * q[T][H*hd]; K,V [T][KV][key_stride][hd]; n_keys[T]; keys cut in `chunk`-key
- * chunks (combined in chunk order) -> o[T][H*hd]. */
+/* Decode attention over a dense per-token K/V (the streamed form of
+ * DESIGN.md 3.3 = oracle or_attention with chunk = -split_keys):
+ * q[T][H*hd]; K,V [T][KV][key_stride][hd]; n_keys[T] (1..key_stride); keys
+ * cut in splits of split_keys (a multiple of 64), each streamed as 4
+ * round-robin 16-key block streams, splits combined in order -> o[T][H*hd].
+ * H/KV <= 16.  Blocking; MG_ERR_INVALID on bad sizes. */
 mg_status mgd_attention(const uint16_t* q, const uint16_t* K, const uint16_t* V, const int32_t* n_keys, int32_t T,
-                        int32_t H, int32_t KV, int32_t hd, int32_t key_stride, int32_t chunk, uint16_t* o,
+                        int32_t H, int32_t KV, int32_t hd, int32_t key_stride, int32_t split_keys, uint16_t* o,
                         void* stream);
 
 /* out[t][i] = bf16(x[t][i] + sum_s part[s][t][i]) */

@@ -183,8 +183,15 @@ void or_qkv_epilogue(const float* acc, const uint16_t* bias, const int32_t* pos,
  * s_j = (q . k_j) * fp32(1/sqrt(hd)); per chunk m = max, e = expf(s - m),
  * l = sum e, acc = sum e*v (left to right); chunks combined in index order
  * with weights expf(m_c - m*); o = bf16(acc / l).  SURVEY 8(c) step 4. */
+static void or_attention_stream(const uint16_t* q, const uint16_t* K, const uint16_t* V, int32_t H, int32_t KV,
+                                int32_t hd, int32_t n, int32_t key_stride, int32_t split_keys, uint16_t* o);
+
 void or_attention(const uint16_t* q, const uint16_t* K, const uint16_t* V, int32_t H, int32_t KV, int32_t hd,
                   int32_t n, int32_t key_stride, int32_t chunk, int32_t splits, uint16_t* o) {
+  if (chunk < 0) {
+    or_attention_stream(q, K, V, H, KV, hd, n, key_stride, -chunk, o);
+    return;
+  }
   int32_t G = H / KV;
   float scale = (float)(1.0 / sqrt((double)hd));
   int64_t nch;
@@ -230,6 +237,81 @@ void or_attention(const uint16_t* q, const uint16_t* K, const uint16_t* V, int32
     free(out);
   }
   free(s); free(mc); free(lc); free(ac);
+}
+
+/* Streamed form of the same attention (reading A14): keys cut
+ * into splits of split_keys; inside a split, 16-key blocks dealt round-robin
+ * to 4 streams (block b -> stream b mod 4).  Each stream keeps a running
+ * (m, l, a) from (-inf, 0, 0); per block, in order:
+ *   m' = max(m, max_j s_j), alpha = expf(m - m'), e_j = expf(s_j - m'),
+ *   l = l*alpha + sum_j e_j,  a = a*alpha + sum_j e_j v_j,  m = m'.
+ * The 4 streams, then the splits, are combined in index order with weights
+ * expf(m_i - max_i m_i); one split: o = bf16(a / l) directly. */
+static void or_attention_stream(const uint16_t* q, const uint16_t* K, const uint16_t* V, int32_t H, int32_t KV,
+                                int32_t hd, int32_t n, int32_t key_stride, int32_t split_keys, uint16_t* o) {
+  int32_t G = H / KV;
+  float scale = (float)(1.0 / sqrt((double)hd));
+  int32_t nsp = (n + split_keys - 1) / split_keys;
+  float* s = (float*)malloc(sizeof(float) * (size_t)n);
+  float* sm = (float*)malloc(sizeof(float) * 4);
+  float* sl = (float*)malloc(sizeof(float) * 4);
+  float* sa = (float*)malloc(sizeof(float) * 4 * hd);
+  float* pm = (float*)malloc(sizeof(float) * (size_t)nsp);
+  float* pl = (float*)malloc(sizeof(float) * (size_t)nsp);
+  float* pa = (float*)malloc(sizeof(float) * (size_t)nsp * hd);
+  for (int32_t h = 0; h < H; ++h) {
+    const uint16_t* Kg = K + (int64_t)(h / G) * key_stride * hd;
+    const uint16_t* Vg = V + (int64_t)(h / G) * key_stride * hd;
+    for (int32_t j = 0; j < n; ++j) s[j] = or_dot_bf16(q + (int64_t)h * hd, Kg + (int64_t)j * hd, hd, 1) * scale;
+    for (int32_t sp = 0; sp < nsp; ++sp) {
+      int32_t lo = sp * split_keys, hi = lo + split_keys < n ? lo + split_keys : n;
+      int32_t nblk = (hi - lo + 15) / 16;
+      for (int32_t w = 0; w < 4; ++w) {
+        float m = -INFINITY, l = 0.0f;
+        float* a = sa + w * hd;
+        for (int32_t d = 0; d < hd; ++d) a[d] = 0.0f;
+        for (int32_t b = w; b < nblk; b += 4) {
+          int32_t j0 = lo + 16 * b, j1 = j0 + 16 < hi ? j0 + 16 : hi;
+          float mn = m;
+          for (int32_t j = j0; j < j1; ++j) mn = s[j] > mn ? s[j] : mn;
+          float alpha = expf(m - mn);
+          float lb = 0.0f;
+          for (int32_t j = j0; j < j1; ++j) lb = lb + expf(s[j] - mn);
+          l = l * alpha + lb;
+          for (int32_t d = 0; d < hd; ++d) {
+            float ab = 0.0f;
+            for (int32_t j = j0; j < j1; ++j) ab = ab + expf(s[j] - mn) * bf(Vg[(int64_t)j * hd + d]);
+            a[d] = a[d] * alpha + ab;
+          }
+          m = mn;
+        }
+        sm[w] = m; sl[w] = l;
+      }
+      float M = -INFINITY;
+      for (int32_t w = 0; w < 4; ++w) M = sm[w] > M ? sm[w] : M;
+      pl[sp] = 0.0f;
+      for (int32_t d = 0; d < hd; ++d) pa[(int64_t)sp * hd + d] = 0.0f;
+      for (int32_t w = 0; w < 4; ++w) {
+        float wt = expf(sm[w] - M);
+        pl[sp] = pl[sp] + sl[w] * wt;
+        for (int32_t d = 0; d < hd; ++d) pa[(int64_t)sp * hd + d] = pa[(int64_t)sp * hd + d] + sa[w * hd + d] * wt;
+      }
+      pm[sp] = M;
+    }
+    if (nsp == 1) {
+      for (int32_t d = 0; d < hd; ++d) o[(int64_t)h * hd + d] = or_f32_to_bf16(pa[d] / pl[0]);
+      continue;
+    }
+    float M = -INFINITY, L = 0.0f;
+    for (int32_t sp = 0; sp < nsp; ++sp) M = pm[sp] > M ? pm[sp] : M;
+    for (int32_t sp = 0; sp < nsp; ++sp) L = L + pl[sp] * expf(pm[sp] - M);
+    for (int32_t d = 0; d < hd; ++d) {
+      float acc = 0.0f;
+      for (int32_t sp = 0; sp < nsp; ++sp) acc = acc + pa[(int64_t)sp * hd + d] * expf(pm[sp] - M);
+      o[(int64_t)h * hd + d] = or_f32_to_bf16(acc / L);
+    }
+  }
+  free(s); free(sm); free(sl); free(sa); free(pm); free(pl); free(pa);
 }
 
 /* residual: out = bf16(x + acc) (one fp32 add). */

@@ -37,9 +37,11 @@ typedef struct {
  * "chunked_dot").  split_* = number of contiguous K-chunks of a dot
  * product (remainder to the leading chunks), each chunk summed left to
  * right in fp32, chunk partials summed left to right.  Attention keys
- * 0..q are cut either into attn_chunk-sized chunks (attn_chunk > 0) or
- * into attn_splits equal chunks.  noise_amp > 0 adds SPEC's test-only
- * injected logit perturbation, exactly 0 at batch 1. */
+ * 0..q are cut either into attn_chunk-sized chunks (attn_chunk > 0), into
+ * attn_splits equal chunks (attn_chunk == 0), or streamed in splits of
+ * -attn_chunk keys (attn_chunk < 0: or_attention's streamed form).
+ * noise_amp > 0 adds SPEC's test-only injected logit perturbation
+ * (SPEC.md:76-84), exactly 0 at batch 1. */
 typedef struct {
   int32_t split_qkv, split_o, split_gu, split_down, split_lm;
   int32_t attn_chunk, attn_splits;
@@ -69,6 +71,8 @@ void or_qkv_epilogue(const float* acc /* [T][(H+2KV)*hd] */, const uint16_t* bia
 void or_attention(const uint16_t* q /* [H][hd] */, const uint16_t* K /* [KV][n][hd] */,
                   const uint16_t* V, int32_t H, int32_t KV, int32_t hd, int32_t n_keys,
                   int32_t key_stride /* >= n_keys */, int32_t chunk, int32_t splits, uint16_t* o /* [H*hd] */);
+/* chunk < 0 selects the streamed form (or_attention_stream) with
+ * split_keys = -chunk; see DESIGN.md 3.3 / A14. */
 void or_residual(const uint16_t* x, const float* acc, int64_t n, uint16_t* out);
 void or_swiglu(const float* g, const float* u, int64_t n, uint16_t* out);
 /* top-2 under the total order (value desc, id asc); NaN ranks as -inf and

@@ -1,27 +1,34 @@
 // attention.cu -- paged GQA decode attention.
 //
-// k_attn_chunk<HD, NB>: one CTA (4 warps) per (token, kv head, key chunk of
-// 64*NB keys).  The G = H/KV query heads sharing the kv head form the 16-row
-// M side of mma.sync.m16n8k16 tiles (rows >= G are zero), so every K/V byte
-// of the chunk is read from HBM once per token.  Keys come in 16-key blocks
-// (a block never crosses a KV page); warp w owns blocks w, w+4, ...  At kernel
-// start every warp issues ALL its K and V rows as 256-byte cp.async.bulk
-// copies (one mbarrier for K, one for V; rows padded to HD*2+16 bytes so the
-// ldmatrix reads are bank-conflict free), so one HBM round trip per CTA is
-// exposed and the V stream overlaps the score phase.  The chunk follows
-// DESIGN.md 3.3 exactly, in two passes:
-//   pass 1  s_j = (q . k_j) * fp32(1/sqrt(hd))  (bf16 x bf16 products, fp32 acc)
-//   softmax m = max_j s_j, e_j = expf(s_j - m), l = sum_j e_j (fixed trees)
-//   pass 2  acc = sum_j e_j v_j  with e split as bf16 hi + bf16 lo (16+ bit
-//           mantissa) so the probabilities are not rounded to bf16
-// then the 4 warps' partial sums are added in warp order.
-// k_attn_combine: chunks combined in chunk order with weights
-// expf(m_c - m*), o = bf16(acc / l).
+// k_attn<HD, R>: one CTA (4 warps) per (token, kv head, key split).  The
+// G = H/KV query heads sharing the kv head form the 16-row M side of
+// mma.sync.m16n8k16 tiles (rows >= G are don't-care: an MMA output row depends
+// only on its own A row), so every K/V byte is read from HBM once per token.
 //
-// Schedules: the fast path uses 64-key chunks (most CTAs, best at every batch
-// size measured); the verifier uses pinned 128-key chunks (A14), so
-// a query's result depends only on its own keys: the block/warp structure is
-// a function of the chunk bounds alone.
+// Arithmetic = the streamed form of DESIGN.md 3.3 (oracle or_attention with
+// chunk = -split_keys): the split's 16-key blocks are dealt round-robin to the
+// 4 warps (block b -> warp b mod 4; a block never crosses a KV page).  Each
+// warp streams its blocks with a running (m, l, acc) per query head:
+//   s_j = (q . k_j) * fp32(1/sqrt(hd))              QK^T on the tensor cores
+//   m' = max(m, max_j s_j), alpha = expf(m - m'),   row max by quad shuffles
+//   e_j = expf(s_j - m'), l = l*alpha + sum_j e_j, acc = acc*alpha + sum_j e_j v_j
+// with e_j fed to the PV MMA as bf16 hi + bf16 lo (16+ bit mantissa) straight
+// from the score registers (the m16n8 C layout of two key tiles IS the m16k16
+// A layout), so scores and probabilities never touch shared memory.  The 4
+// warps are then combined in warp order with weights expf(m_w - max m); a
+// token with one split writes o = bf16(acc / l); otherwise each split writes
+// (acc, m, l) and the LAST CTA of the (token, kv head) to arrive (atomic
+// counter, reset by it) combines the splits in split order.  Every choice is
+// a function of (n_keys, split_keys) alone, so with a pinned split_keys (the
+// verifier) a query's result does not depend on the batch.
+//
+// Data movement: TMA only.  Each warp owns a ring of R stages (K block + V
+// block, box 64 dims x 16 keys, 128B swizzle -> conflict-free ldmatrix) that
+// its lane 0 refills as soon as the warp has consumed a stage; warp 0 loads
+// the Q tile once.  Page-table lookups for 32 blocks at a time are done by the
+// 32 lanes in parallel and shuffled to lane 0 at issue time.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -29,24 +36,21 @@ namespace mg {
 
 constexpr int kAtThreads = 128;
 
-template <int HD, int NB>
+template <int HD, int R>
 struct AtCfg {
-  static constexpr int ROWB = HD * 2 + 16;
-  static constexpr int BLKB = 16 * ROWB;
-  static constexpr int CH = 64 * NB;                  // keys per chunk
-  static constexpr int S_BYTES = 16 * CH * 4;
-  static constexpr int KV_BYTES = 2 * 4 * NB * BLKB;  // [K|V][warp][NB] blocks
-  static constexpr int X_BYTES = 4 * 16 * HD * 4;     // cross-warp sums, aliases the K/V region
-  static_assert(X_BYTES <= KV_BYTES, "reduction scratch must fit in the K/V region");
-  static constexpr int SMEM = S_BYTES + KV_BYTES + 4 * 16 * 4 + 32 * 4 + 8 * 8;
+  static constexpr int HALVES = HD / 64;
+  static constexpr int BLK = HALVES * 2048;        // one 16-row tile: HALVES x [16][128 B] swizzled
+  static constexpr int STAGE = 2 * BLK;            // K block + V block
+  static constexpr int XST = HD + 8;               // cross-warp scratch row stride (floats)
+  static constexpr int RING = 4 * R * STAGE;
+  static constexpr int XG = 4 * 16 * XST * 4;      // [warp][16][XST] fp32, aliases the rings
+  static constexpr int Q_OFF = 0;
+  static constexpr int RING_OFF = BLK;
+  static constexpr int ML_OFF = RING_OFF + (RING > XG ? RING : XG);  // m, l: [warp][16] each
+  static constexpr int BAR_OFF = ML_OFF + 2 * 64 * 4;                 // Q, then [warp][R]
+  static constexpr int SMEM = BAR_OFF + (1 + 4 * R) * 8 + 8 + 1024;   // + flag + alignment slack
 };
 
-MG_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 MG_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -64,247 +68,288 @@ MG_DEV void mma_bf16(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// byte offset of the 16-byte chunk holding (row r, column col) of a TMA tile
+// stored as HD/64 halves of [16 rows][128 B] with the 128B swizzle
+MG_DEV uint32_t swz(int r, int col) {
+  return (uint32_t)((col >> 6) * 2048 + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4));
+}
+// hi/lo bf16 pair of two fp32 probabilities: hi = bf16(e), lo = bf16(e - hi)
+MG_DEV void split_pair(float e0, float e1, uint32_t& hi, uint32_t& lo) {
+  hi = pack_bf2(e0, e1);
+  lo = pack_bf2(__fsub_rn(e0, lo_bf(hi)), __fsub_rn(e1, hi_bf(hi)));
+}
 
-template <int HD, int NB>
-__global__ void __launch_bounds__(kAtThreads) k_attn_chunk(AttnArgs a) {
-  using C = AtCfg<HD, NB>;
-  extern __shared__ __align__(16) uint8_t sm[];
-  float* S = reinterpret_cast<float*>(sm);                                // [16][CH]
-  uint8_t* kvr = sm + C::S_BYTES;                                         // K/V blocks
-  float* red = reinterpret_cast<float*>(sm + C::S_BYTES + C::KV_BYTES);  // [4][16]
-  float* s_ml = red + 4 * 16;                                             // m[16], l[16]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_ml + 32);                // [K 4][V 4]
+template <int HD, int R>
+__global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ AttnArgs a) {
+  using C = AtCfg<HD, R>;
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
+  float* s_m = reinterpret_cast<float*>(sm + C::ML_OFF);  // [warp][16]
+  float* s_l = s_m + 64;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  int* s_flag = reinterpret_cast<int*>(bars + 1 + 4 * R);
 
-  const int t = blockIdx.x, kvh = blockIdx.y, c = blockIdx.z;
+  const int t = blockIdx.x, kvh = blockIdx.y, sp = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.H, G = a.H / a.KV;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 1 + 4 * R; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
   griddep();
   const int n = a.n_keys[t];
-  const int lo = c * C::CH;
-  const size_t po = ((size_t)t * H + (size_t)kvh * G) * a.n_chunks + c;
-  if (lo >= n) {
-    if (threadIdx.x < G) {
-      a.part_ml[(po + (size_t)threadIdx.x * a.n_chunks) * 2 + 0] = -INFINITY;
-      a.part_ml[(po + (size_t)threadIdx.x * a.n_chunks) * 2 + 1] = 0.f;
-    }
-    return;
-  }
-  const int hi = min(n, lo + C::CH);
-  const int len = hi - lo;
-  const int nblk = (len + 15) >> 4;
-  const int nbw = nblk > warp ? min(NB, (nblk - warp + 3) >> 2) : 0;  // blocks of this warp
+  const int lo = sp * a.split_keys;
+  if (lo >= n) return;
+  const int hi = min(n, lo + a.split_keys);
+  const int nblk = (hi - lo + 15) >> 4;
+  const int nbw = nblk > warp ? (nblk - warp + 3) >> 2 : 0;  // blocks of this warp
+  const int n_sp = (n + a.split_keys - 1) / a.split_keys;
+  uint8_t* ring = sm + C::RING_OFF + warp * R * C::STAGE;
+  uint64_t* full = bars + 1 + warp * R;
 
-  // ---- issue every K and V row of this warp's blocks (one round trip)
-  {
-    const int slot = a.paged ? a.slot[t] : 0;
-    auto krow = [&](int j, int kvsel) -> const uint16_t* {
+  // ---- TMA issue: Q tile (warp 0), then the first R blocks of each warp
+  int my_sl = 0, my_row = 0;  // lane j: coordinates of this warp's block (32*batch + j)
+  auto coords = [&](int base) {
+    const int i = base + lane;
+    if (i < nbw) {
+      const int key0 = lo + 16 * (warp + 4 * i);
       if (a.paged) {
         const CacheView& cv = a.cache;
-        const int page = cv.pt[(size_t)slot * cv.max_pages + j / cv.page_size];
-        return cv.pool + ((((size_t)cv.layer * cv.n_pages + page) * 2 + kvsel) * cv.kv + kvh) *
-                             (size_t)cv.page_size * HD +
-               (size_t)(j % cv.page_size) * HD;
-      }
-      const uint16_t* base = kvsel ? a.Vd : a.Kd;
-      return base + (((size_t)t * a.KV + kvh) * a.key_stride + j) * HD;
-    };
-    int valid_rows = 0;
-    for (int j = 0; j < nbw; ++j) valid_rows += min(16, hi - (lo + 16 * (warp + 4 * j)));
-    if (lane == 0) {
-      mbar_expect_tx(&bars[warp], (uint32_t)valid_rows * HD * 2);
-      mbar_expect_tx(&bars[4 + warp], (uint32_t)valid_rows * HD * 2);
-    }
-    __syncwarp();
-    for (int e = lane; e < nbw * 32; e += 32) {
-      const int j = e >> 5, kvsel = (e >> 4) & 1, r = e & 15;
-      const int key = lo + 16 * (warp + 4 * j) + r;
-      uint8_t* dst = kvr + ((size_t)(kvsel * 4 + warp) * NB + j) * C::BLKB + r * C::ROWB;
-      if (key < hi) {
-        bulk_g2s(dst, krow(key, kvsel), HD * 2, &bars[kvsel * 4 + warp]);
+        const int page = cv.pt[(size_t)a.slot[t] * cv.max_pages + key0 / cv.page_size];
+        my_sl = (cv.layer * cv.n_pages + page) * 2 * a.KV + kvh;
+        my_row = key0 % cv.page_size;
       } else {
-        for (int q = 0; q < HD / 8; ++q) reinterpret_cast<uint4*>(dst)[q] = make_uint4(0, 0, 0, 0);
+        my_sl = t * a.KV + kvh;
+        my_row = key0;
       }
     }
-  }
-
-  // ---- Q fragments (A operand, rows = query heads of this kv head, zero-padded)
-  const int r0 = lane >> 2, r1 = r0 + 8, cc = 2 * (lane & 3);
-  const uint16_t* qp = a.q + (size_t)t * H * HD + (size_t)kvh * G * HD;
-  uint32_t qf[HD / 16][4];
+  };
+  const int vsl = a.paged ? a.KV : 0;  // V slab offset inside the pool map
+  auto issue = [&](int i) {            // warp-wide (shuffles); lane 0 issues
+    const int sl = __shfl_sync(0xffffffffu, my_sl, i & 31), row = __shfl_sync(0xffffffffu, my_row, i & 31);
+    if (lane == 0) {
+      const int s = i % R;
+      uint8_t* st = ring + s * C::STAGE;
+      mbar_expect_tx(&full[s], C::STAGE);
 #pragma unroll
-  for (int ks = 0; ks < HD / 16; ++ks) {
-    const int k0 = ks * 16 + cc;
-    qf[ks][0] = r0 < G ? *reinterpret_cast<const uint32_t*>(qp + r0 * HD + k0) : 0u;
-    qf[ks][1] = r1 < G ? *reinterpret_cast<const uint32_t*>(qp + r1 * HD + k0) : 0u;
-    qf[ks][2] = r0 < G ? *reinterpret_cast<const uint32_t*>(qp + r0 * HD + k0 + 8) : 0u;
-    qf[ks][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(qp + r1 * HD + k0 + 8) : 0u;
+      for (int h = 0; h < C::HALVES; ++h) tma_load_3d(st + h * 2048, &a.kmap, &full[s], 64 * h, row, sl);
+#pragma unroll
+      for (int h = 0; h < C::HALVES; ++h)
+        tma_load_3d(st + C::BLK + h * 2048, &a.vmap, &full[s], 64 * h, row, sl + vsl);
+    }
+  };
+  if (warp == 0 && lane == 0) {
+    mbar_expect_tx(&bars[0], C::BLK);
+#pragma unroll
+    for (int h = 0; h < C::HALVES; ++h) tma_load_3d(sm + C::Q_OFF + h * 2048, &a.qmap, &bars[0], 64 * h, kvh * G, t);
   }
+  coords(0);
+  for (int i = 0; i < R && i < nbw; ++i) issue(i);
+
+  const int rr = lane & 7, mi = lane >> 3;
+  const int r0 = lane >> 2, r1 = r0 + 8, cc = 2 * (lane & 3);
+  // ---- Q tile (A operand; rows >= G are other heads / zero fill, ignored).
+  // Its fragments are re-read from shared memory per block (ldmatrix) rather
+  // than held in registers, which keeps the kernel at 4 CTAs per SM.
+  mbar_wait(&bars[0], 0);
+  const uint32_t qa = smem_u32(sm + C::Q_OFF);
   const float scale = (float)(1.0 / sqrt((double)HD));
 
-  // ---- pass 1: scores
-  __syncwarp();
-  mbar_wait(&bars[warp], 0);
-  for (int j = 0; j < nbw; ++j) {
-    const uint32_t kb = smem_u32(kvr + ((size_t)warp * NB + j) * C::BLKB);
-    const int b = warp + 4 * j;
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      float sacc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int kg = 0; kg < HD / 32; ++kg) {
-        uint32_t b0, b1, b2, b3;
-        const int mi = lane >> 3, rr = lane & 7;
-        ldsm_x4(kb + (8 * nt + rr) * C::ROWB + (32 * kg + 8 * mi) * 2, b0, b1, b2, b3);
-        mma_bf16(sacc, qf[2 * kg], b0, b1);
-        mma_bf16(sacc, qf[2 * kg + 1], b2, b3);
-      }
-      const int j0 = 16 * b + 8 * nt + cc;  // key index within the chunk
-      const bool v0 = lo + j0 < hi, v1 = lo + j0 + 1 < hi;
-      S[r0 * C::CH + j0] = v0 ? __fmul_rn(sacc[0], scale) : -INFINITY;
-      S[r0 * C::CH + j0 + 1] = v1 ? __fmul_rn(sacc[1], scale) : -INFINITY;
-      S[r1 * C::CH + j0] = v0 ? __fmul_rn(sacc[2], scale) : -INFINITY;
-      S[r1 * C::CH + j0 + 1] = v1 ? __fmul_rn(sacc[3], scale) : -INFINITY;
-    }
-  }
-  __syncthreads();
-
-  // ---- softmax over the chunk: query head g is owned by warp g % 4, lane l
-  // takes keys l, l+32, ... (fixed trees, no CTA-wide barrier per head)
-  for (int g = warp; g < G; g += 4) {
-    float* sg = S + g * C::CH;
-    float m = -INFINITY;
-    for (int j = lane; j < len; j += 32) m = fmaxf(m, sg[j]);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    float l = 0.f;
-    for (int j = lane; j < C::CH; j += 32) {
-      const float e = j < len ? expf(__fsub_rn(sg[j], m)) : 0.f;
-      sg[j] = e;
-      l = __fadd_rn(l, e);
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) l = __fadd_rn(l, __shfl_xor_sync(0xffffffffu, l, off));
-    if (lane == 0) {
-      s_ml[g] = m;
-      s_ml[16 + g] = l;
-    }
-  }
-  __syncthreads();
-
-  // ---- pass 2: acc = sum_j e_j v_j  (e = hi + lo, two bf16 MMAs).  Warp w owns
-  // head dims [w*HD/4, (w+1)*HD/4) and sums ALL the chunk's key blocks in order,
-  // so no cross-warp reduction is needed.
-  constexpr int NT = HD / 32;  // 8-dim n-tiles per warp
+  // ---- stream this warp's blocks
+  constexpr int NT = HD / 8;  // 8-dim n-tiles of the output
   float acc[NT][4];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
-  for (int w = 0; w < 4; ++w) mbar_wait(&bars[4 + w], 0);  // every warp's V rows landed
-  const int d0 = warp * (HD / 4);
-  for (int b = 0; b < nblk; ++b) {
-    const uint32_t vb = smem_u32(kvr + ((size_t)(4 + (b & 3)) * NB + (b >> 2)) * C::BLKB);
-    const int j0 = 16 * b;
-    uint32_t ph[4], pl[4];
-    {
-      const float* s0 = S + r0 * C::CH + j0 + cc;
-      const float* s1 = S + r1 * C::CH + j0 + cc;
-      const bool g0 = r0 < G, g1 = r1 < G;  // rows >= G are padding: P = 0
-      const float e[8] = {g0 ? s0[0] : 0.f, g0 ? s0[1] : 0.f, g1 ? s1[0] : 0.f, g1 ? s1[1] : 0.f,
-                          g0 ? s0[8] : 0.f, g0 ? s0[9] : 0.f, g1 ? s1[8] : 0.f, g1 ? s1[9] : 0.f};
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows r0, r1 (l: this lane's keys)
+  for (int i = 0; i < nbw; ++i) {
+    const int s = i % R;
+    mbar_wait(&full[s], (uint32_t)((i / R) & 1));
+    uint8_t* st = ring + s * C::STAGE;
+    const uint32_t kb = smem_u32(st), vb = kb + C::BLK;
+    const int valid = min(16, hi - (lo + 16 * (warp + 4 * i)));
+    if (valid < 16) {  // the split's last block: zero V rows past the end (P is 0 there)
+      for (int e = lane; e < (16 - valid) * C::HALVES * 8; e += 32) {
+        const int row = valid + e / (C::HALVES * 8), rem = e % (C::HALVES * 8);
+        reinterpret_cast<uint4*>(st + C::BLK + (rem >> 3) * 2048 + row * 128)[rem & 7] = make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+    }
+    // scores: two 8-key tiles
+    float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t h = pack_bf2(e[2 * q], e[2 * q + 1]);
-        ph[q] = h;
-        pl[q] = pack_bf2(__fsub_rn(e[2 * q], lo_bf(h)), __fsub_rn(e[2 * q + 1], hi_bf(h)));
+    for (int kg = 0; kg < HD / 32; ++kg) {
+      uint32_t q0[4], q1[4];
+      ldsm_x4(qa + swz((mi & 1) * 8 + rr, 32 * kg + 8 * (mi >> 1)), q0[0], q0[1], q0[2], q0[3]);
+      ldsm_x4(qa + swz((mi & 1) * 8 + rr, 32 * kg + 16 + 8 * (mi >> 1)), q1[0], q1[1], q1[2], q1[3]);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(kb + swz(8 * nt + rr, 32 * kg + 8 * mi), b0, b1, b2, b3);
+        mma_bf16(sc[nt], q0, b0, b1);
+        mma_bf16(sc[nt], q1, b2, b3);
       }
     }
 #pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        sc[nt][q] = 8 * nt + cc + (q & 1) < valid ? __fmul_rn(sc[nt][q], scale) : -INFINITY;
+    float b0m = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
+    float b1m = fmaxf(fmaxf(sc[0][2], sc[0][3]), fmaxf(sc[1][2], sc[1][3]));
+    b0m = fmaxf(b0m, __shfl_xor_sync(0xffffffffu, b0m, 1));
+    b1m = fmaxf(b1m, __shfl_xor_sync(0xffffffffu, b1m, 1));
+    b0m = fmaxf(b0m, __shfl_xor_sync(0xffffffffu, b0m, 2));
+    b1m = fmaxf(b1m, __shfl_xor_sync(0xffffffffu, b1m, 2));
+    const float n0 = fmaxf(m0, b0m), n1 = fmaxf(m1, b1m);
+    const float al0 = expf(__fsub_rn(m0, n0)), al1 = expf(__fsub_rn(m1, n1));
+    m0 = n0;
+    m1 = n1;
+    float e[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      e[nt][0] = expf(__fsub_rn(sc[nt][0], n0));
+      e[nt][1] = expf(__fsub_rn(sc[nt][1], n0));
+      e[nt][2] = expf(__fsub_rn(sc[nt][2], n1));
+      e[nt][3] = expf(__fsub_rn(sc[nt][3], n1));
+    }
+    l0 = __fadd_rn(__fmul_rn(l0, al0), __fadd_rn(__fadd_rn(e[0][0], e[0][1]), __fadd_rn(e[1][0], e[1][1])));
+    l1 = __fadd_rn(__fmul_rn(l1, al1), __fadd_rn(__fadd_rn(e[0][2], e[0][3]), __fadd_rn(e[1][2], e[1][3])));
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      acc[nt][0] = __fmul_rn(acc[nt][0], al0);
+      acc[nt][1] = __fmul_rn(acc[nt][1], al0);
+      acc[nt][2] = __fmul_rn(acc[nt][2], al1);
+      acc[nt][3] = __fmul_rn(acc[nt][3], al1);
+    }
+    uint32_t ph[4], pl[4];
+    split_pair(e[0][0], e[0][1], ph[0], pl[0]);  // row r0, keys cc, cc+1
+    split_pair(e[0][2], e[0][3], ph[1], pl[1]);  // row r1, keys cc, cc+1
+    split_pair(e[1][0], e[1][1], ph[2], pl[2]);  // row r0, keys 8+cc
+    split_pair(e[1][2], e[1][3], ph[3], pl[3]);  // row r1, keys 8+cc
+#pragma unroll
     for (int n2 = 0; n2 < NT / 2; ++n2) {
       uint32_t b0, b1, b2, b3;
-      const int mi = lane >> 3, rr = lane & 7;
-      ldsm_x4_t(vb + ((mi & 1) * 8 + rr) * C::ROWB + (d0 + 16 * n2 + 8 * (mi >> 1)) * 2, b0, b1, b2, b3);
+      ldsm_x4_t(vb + swz((mi & 1) * 8 + rr, 16 * n2 + 8 * (mi >> 1)), b0, b1, b2, b3);
       mma_bf16(acc[2 * n2], ph, b0, b1);
       mma_bf16(acc[2 * n2], pl, b0, b1);
       mma_bf16(acc[2 * n2 + 1], ph, b2, b3);
       mma_bf16(acc[2 * n2 + 1], pl, b2, b3);
     }
+    if (i + R < nbw) {  // refill the stage just consumed
+      __syncwarp();
+      fence_proxy_async();
+      if (((i + R) & 31) == 0) coords(i + R);
+      issue(i + R);
+    }
   }
-  // ---- write the chunk partials (rows < G)
+  // lane partial sums -> row sums (fixed butterfly, the same in all 4 lanes)
+  l0 = __fadd_rn(l0, __shfl_xor_sync(0xffffffffu, l0, 1));
+  l1 = __fadd_rn(l1, __shfl_xor_sync(0xffffffffu, l1, 1));
+  l0 = __fadd_rn(l0, __shfl_xor_sync(0xffffffffu, l0, 2));
+  l1 = __fadd_rn(l1, __shfl_xor_sync(0xffffffffu, l1, 2));
+
+  // ---- combine the 4 warps (streams) in warp order
+  __syncthreads();  // every ring consumed: the scratch may alias them
+  float* X = reinterpret_cast<float*>(sm + C::RING_OFF);
+  if ((lane & 3) == 0) {
+    s_m[warp * 16 + r0] = m0;
+    s_m[warp * 16 + r1] = m1;
+    s_l[warp * 16 + r0] = l0;
+    s_l[warp * 16 + r1] = l1;
+  }
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    const int d = d0 + 8 * nt + cc;
-    if (r0 < G) {
-      float* o = a.part_acc + (po + (size_t)r0 * a.n_chunks) * HD + d;
-      *reinterpret_cast<float2*>(o) = make_float2(acc[nt][0], acc[nt][1]);
+    const int d = 8 * nt + cc;
+    if (r0 < G) *reinterpret_cast<float2*>(X + (warp * 16 + r0) * C::XST + d) = make_float2(acc[nt][0], acc[nt][1]);
+    if (r1 < G) *reinterpret_cast<float2*>(X + (warp * 16 + r1) * C::XST + d) = make_float2(acc[nt][2], acc[nt][3]);
+  }
+  __syncthreads();
+  const size_t obase = ((size_t)t * H + (size_t)kvh * G) * HD;
+  const size_t pbase = ((size_t)t * H + (size_t)kvh * G) * a.n_splits + sp;  // + g * n_splits
+  for (int e = threadIdx.x; e < G * HD; e += kAtThreads) {
+    const int g = e / HD, d = e % HD;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, s_m[w * 16 + g]);
+    float L = 0.f, A = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float wt = expf(__fsub_rn(s_m[w * 16 + g], M));
+      L = __fadd_rn(L, __fmul_rn(s_l[w * 16 + g], wt));
+      A = __fadd_rn(A, __fmul_rn(X[(w * 16 + g) * C::XST + d], wt));
     }
-    if (r1 < G) {
-      float* o = a.part_acc + (po + (size_t)r1 * a.n_chunks) * HD + d;
-      *reinterpret_cast<float2*>(o) = make_float2(acc[nt][2], acc[nt][3]);
+    if (n_sp == 1) {
+      a.out[obase + (size_t)g * HD + d] = f2bf(__fdiv_rn(A, L));
+    } else {
+      const size_t p = pbase + (size_t)g * a.n_splits;
+      a.part_acc[p * HD + d] = A;
+      if (d == 0) {
+        a.part_ml[p * 2 + 0] = M;
+        a.part_ml[p * 2 + 1] = L;
+      }
     }
   }
-  if (threadIdx.x < G) {
-    const size_t o = po + (size_t)threadIdx.x * a.n_chunks;
-    a.part_ml[o * 2 + 0] = s_ml[threadIdx.x];
-    a.part_ml[o * 2 + 1] = s_ml[16 + threadIdx.x];
+  if (n_sp == 1) return;
+
+  // ---- several splits: the last CTA to arrive combines them in split order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t* cnt = a.counter + (size_t)t * a.KV + kvh;
+    const int last = atomicAdd(cnt, 1) == n_sp - 1;
+    if (last) *cnt = 0;
+    *s_flag = last;
+  }
+  __syncthreads();
+  if (!*s_flag) return;
+  __threadfence();
+  for (int e = threadIdx.x; e < G * HD; e += kAtThreads) {
+    const int g = e / HD, d = e % HD;
+    const size_t base = ((size_t)t * H + (size_t)kvh * G + g) * a.n_splits;
+    float M = -INFINITY;
+    for (int k = 0; k < n_sp; ++k) M = fmaxf(M, __ldcg(a.part_ml + (base + k) * 2));
+    float L = 0.f;
+    for (int k = 0; k < n_sp; ++k)
+      L = __fadd_rn(L, __fmul_rn(__ldcg(a.part_ml + (base + k) * 2 + 1),
+                                 expf(__fsub_rn(__ldcg(a.part_ml + (base + k) * 2), M))));
+    float A = 0.f;
+    for (int k = 0; k < n_sp; ++k)
+      A = __fadd_rn(A, __fmul_rn(__ldcg(a.part_acc + (base + k) * HD + d),
+                                 expf(__fsub_rn(__ldcg(a.part_ml + (base + k) * 2), M))));
+    a.out[obase + (size_t)g * HD + d] = f2bf(__fdiv_rn(A, L));
   }
 }
 
-// grid (T, H), block hd
-__global__ void k_attn_combine(const float* __restrict__ part_acc, const float* __restrict__ part_ml,
-                               const int32_t* __restrict__ n_keys, int H, int hd, int chunk, int n_chunks,
-                               uint16_t* __restrict__ out) {
-  griddep();
-  const int t = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
-  const int nch = (n_keys[t] + chunk - 1) / chunk;
-  const size_t base = ((size_t)t * H + h) * n_chunks;
-  float ms = -INFINITY;
-  for (int c = 0; c < nch; ++c) ms = fmaxf(ms, part_ml[(base + c) * 2]);
-  float L = 0.f, acc = 0.f;
-  for (int c = 0; c < nch; ++c) {
-    const float w = expf(__fsub_rn(part_ml[(base + c) * 2], ms));
-    L = __fadd_rn(L, __fmul_rn(part_ml[(base + c) * 2 + 1], w));
-    acc = __fadd_rn(acc, __fmul_rn(part_acc[(base + c) * hd + d], w));
-  }
-  out[(size_t)t * H * hd + (size_t)h * hd + d] = f2bf(__fdiv_rn(acc, L));
-}
-
-template <int HD, int NB>
+template <int HD, int R>
 static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_attn_chunk<HD, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         AtCfg<HD, NB>::SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_attn<HD, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, AtCfg<HD, R>::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_k(k_attn_chunk<HD, NB>, dim3(a.T, a.KV, a.n_chunks), dim3(kAtThreads), AtCfg<HD, NB>::SMEM, st, a);
+  return launch_k(k_attn<HD, R>, dim3(a.T, a.KV, a.n_splits), dim3(kAtThreads), AtCfg<HD, R>::SMEM, st, a);
 }
 
-int attn_max_chunk() { return 256; }
+// ring depth: 2 stages per warp while the grid fits ~3 CTAs per SM, else 1
+// (more CTAs resident; the other warps of the SM cover the latency).
+// MG_ATTN_RING=1|2 forces it (measurement only).
+static int g_attn_ring = 0;
 
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st) {
-  if (a.H / a.KV > 16 || a.H % a.KV) return cudaErrorInvalidValue;
-  cudaError_t e;
-  if (a.hd == 128) {
-    if (a.chunk == 64) e = launch_attn_t<128, 1>(a, st);
-    else if (a.chunk == 128) e = launch_attn_t<128, 2>(a, st);
-    else if (a.chunk == 256) e = launch_attn_t<128, 4>(a, st);
-    else return cudaErrorInvalidValue;
-  } else if (a.hd == 64) {
-    if (a.chunk == 64) e = launch_attn_t<64, 1>(a, st);
-    else if (a.chunk == 128) e = launch_attn_t<64, 2>(a, st);
-    else if (a.chunk == 256) e = launch_attn_t<64, 4>(a, st);
-    else return cudaErrorInvalidValue;
-  } else {
+  if (a.H % a.KV || a.H / a.KV > 16 || !a.counter || a.split_keys < 64 || a.split_keys % 64 || a.n_splits < 1)
     return cudaErrorInvalidValue;
+  if (!g_attn_ring) {
+    const char* s = getenv("MG_ATTN_RING");
+    g_attn_ring = s && (atoi(s) == 1 || atoi(s) == 2) ? atoi(s) : -1;
   }
-  if (e != cudaSuccess) return e;
-  return launch_k(k_attn_combine, dim3(a.T, a.H), dim3(a.hd), 0, st, (const float*)a.part_acc,
-                  (const float*)a.part_ml, a.n_keys, a.H, a.hd, a.chunk, a.n_chunks, a.out);
+  const long ctas = (long)a.T * a.KV * a.n_splits;
+  const int R = g_attn_ring > 0 ? g_attn_ring : (ctas <= 3L * num_sms() ? 2 : 1);
+  if (a.hd == 128) return R == 2 ? launch_attn_t<128, 2>(a, st) : launch_attn_t<128, 1>(a, st);
+  if (a.hd == 64) return R == 2 ? launch_attn_t<64, 2>(a, st) : launch_attn_t<64, 1>(a, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace mg

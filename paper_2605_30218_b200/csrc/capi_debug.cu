@@ -32,7 +32,8 @@ mg_status mgd_gemm(const uint16_t* x, const uint16_t* W, int32_t T, int32_t N, i
                    int32_t impl, int32_t mma_n, int32_t tile_n, float* out, void* stream) {
   // splits < 0: stream-K over G = -splits virtual CTAs (tcgen05 only)
   const int G = splits < 0 ? -splits : 0;
-  if (!x || !W || !out || T < 1 || N % 128 || K % 64 || splits == 0 || splits > K / 64 || G > 4096)
+  if (!x || !W || !out || T < 1 || N % 128 || K % 64 || splits == 0 || splits > K / 64 ||
+      G > (N / 128) * (K / 64))
     return MG_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
   if (impl != 1) {
@@ -94,24 +95,32 @@ mg_status mgd_qkv_epilogue(const float* part, int32_t splits, const uint16_t* bi
 }
 
 mg_status mgd_attention(const uint16_t* q, const uint16_t* K, const uint16_t* V, const int32_t* n_keys, int32_t T,
-                        int32_t H, int32_t KVh, int32_t hd, int32_t key_stride, int32_t chunk, uint16_t* o,
+                        int32_t H, int32_t KVh, int32_t hd, int32_t key_stride, int32_t split_keys, uint16_t* o,
                         void* stream) {
-  if (!q || !K || !V || !n_keys || !o || T < 1 || chunk < 16 || chunk > 256 || chunk % 16 || key_stride < 1)
+  if (!q || !K || !V || !n_keys || !o || T < 1 || split_keys < 64 || split_keys % 64 || key_stride < 1)
     return MG_ERR_INVALID;
-  const int nch = (key_stride + chunk - 1) / chunk;
+  if (KVh < 1 || H % KVh || H / KVh > 16) return MG_ERR_INVALID;
+  const int nsp = (key_stride + split_keys - 1) / split_keys;
   float *acc = nullptr, *ml = nullptr;
-  if (cudaMalloc(&acc, (size_t)T * H * nch * hd * 4) != cudaSuccess ||
-      cudaMalloc(&ml, (size_t)T * H * nch * 2 * 4) != cudaSuccess)
+  int32_t* cnt = nullptr;
+  if (cudaMalloc(&acc, (size_t)T * H * nsp * hd * 4) != cudaSuccess ||
+      cudaMalloc(&ml, (size_t)T * H * nsp * 2 * 4) != cudaSuccess ||
+      cudaMalloc(&cnt, (size_t)T * KVh * 4) != cudaSuccess)
     return MG_ERR_CUDA;
+  cudaMemset(cnt, 0, (size_t)T * KVh * 4);
   AttnArgs a{};
   a.q = q; a.paged = 0; a.n_keys = n_keys; a.Kd = K; a.Vd = V; a.key_stride = key_stride;
-  a.T = T; a.H = H; a.KV = KVh; a.hd = hd; a.chunk = chunk; a.n_chunks = nch;
-  a.part_acc = acc; a.part_ml = ml; a.out = o;
+  a.T = T; a.H = H; a.KV = KVh; a.hd = hd; a.split_keys = split_keys; a.n_splits = nsp;
+  a.part_acc = acc; a.part_ml = ml; a.counter = cnt; a.out = o;
+  cudaError_t e = cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = launch_attention(a, st);
+  if (make_tmap_3d(&a.qmap, q, hd, H, T, 16) && make_tmap_3d(&a.kmap, K, hd, key_stride, (int64_t)T * KVh, 16) &&
+      make_tmap_3d(&a.vmap, V, hd, key_stride, (int64_t)T * KVh, 16))
+    e = launch_attention(a, st);
   cudaStreamSynchronize(st);
   cudaFree(acc);
   cudaFree(ml);
+  cudaFree(cnt);
   return st_of(e);
 }
 

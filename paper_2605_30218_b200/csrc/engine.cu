@@ -11,8 +11,8 @@
 //   3. gate + compaction + catch-up list; the host reads
 //      the trigger count (the verifier's size is data dependent);
 //   4. verifier on the gated rows, schedule sched_det (pinned split-K per
-//      weight shape, 16-column MMA slot groups, fixed 256-key attention
-//      chunks): the catch-up tokens shadow_len..p run through the same
+//      weight shape, 16-column MMA slot groups, attention splits of a
+//      pinned 512 keys): the catch-up tokens shadow_len..p run through the same
 //      kernels against the SHADOW cache (A1), in chunks of Tv
 //      tokens; the LM head + argmax runs on each gated row's last token;
 //   5. commit: fast / verified / single-column repair
@@ -30,6 +30,7 @@ using namespace mg;
 namespace {
 
 constexpr int kSMs = 148;
+constexpr int kDetSplitKeys = 512;  // verifier attention: keys per split (A14)
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -127,9 +128,13 @@ static Sched sched_fast(const mg_ctx* c, int T, int max_ctx) {
   s.gu = op_fast(2 * c->F, c->d, T);
   s.down = op_fast(c->d, c->F, T);
   s.lm = op_lm(c->V, c->d, T, false);
-  // 64-key chunks: the most CTAs per (token, kv head), best measured at every batch
-  s.attn_chunk = 64;
-  s.attn_nch = cdiv(max_ctx, 64);
+  // attention: one split per (token, kv head) once that fills ~2 CTAs per SM;
+  // smaller batches split the keys (>= 128 per split) to reach that
+  const int ctas = T * c->KV, target = 2 * kSMs;
+  int ns = 1;
+  if (ctas < target) ns = clampi(cdiv(target, ctas), 1, cdiv(max_ctx, 128) > 1 ? cdiv(max_ctx, 128) : 1);
+  s.attn_sk = cdiv(cdiv(max_ctx, ns), 64) * 64;
+  s.attn_ns = cdiv(max_ctx, s.attn_sk);
   return s;
 }
 
@@ -140,8 +145,8 @@ static Sched sched_det(const mg_ctx* c, int T, int max_ctx) {
   s.gu = op_det(2 * c->F, c->d, T);
   s.down = op_det(c->d, c->F, T);
   s.lm = op_lm(c->V, c->d, T, true);
-  s.attn_chunk = 128;  // pinned verifier attention split (A14)
-  s.attn_nch = cdiv(max_ctx, 128);
+  s.attn_sk = kDetSplitKeys;  // pinned verifier attention split (A14)
+  s.attn_ns = cdiv(max_ctx, kDetSplitKeys);
   return s;
 }
 
@@ -207,10 +212,8 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   for (int T = 1; T <= c->Tv; T = T < 16 ? T + 1 : T + 16) upd(sched_det(c, T, g.max_seq), T);
   upd(sched_det(c, c->Tv, g.max_seq), c->Tv);
   c->part_elems = pe;
-  c->nch_max = cdiv(g.max_seq, 16);
-  if (c->nch_max > 512) c->nch_max = 512;
   size_t attn_rows_fast = (size_t)g.max_batch * c->H * cdiv(g.max_seq, 64);
-  size_t attn_rows_det = (size_t)c->Tv * c->H * cdiv(g.max_seq, 128);
+  size_t attn_rows_det = (size_t)c->Tv * c->H * cdiv(g.max_seq, kDetSplitKeys);
   size_t attn_rows = attn_rows_fast > attn_rows_det ? attn_rows_fast : attn_rows_det;
 
   Carver s(ws);
@@ -226,6 +229,7 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   c->logits = s.take<float>((size_t)B * c->V);
   c->attn_acc = s.take<float>(attn_rows * c->hd);
   c->attn_ml = s.take<float>(attn_rows * 2);
+  c->attn_cnt = s.take<int32_t>((size_t)Tm * c->KV);
   c->top2_part = s.take<float>((size_t)Tm * c->nb_top2 * 4);
   c->rope_cos = s.take<float>((size_t)g.max_seq * (c->hd / 2));
   c->rope_sin = s.take<float>((size_t)g.max_seq * (c->hd / 2));
@@ -347,8 +351,9 @@ static mg_status forward(mg_ctx* c, int T, const int32_t* slot, const int32_t* p
                       &cv, slot, nullptr, nullptr, c->st));
     AttnArgs aa{};
     aa.q = c->q; aa.cache = cv; aa.paged = 1; aa.slot = slot; aa.n_keys = nk;
-    aa.T = T; aa.H = c->H; aa.KV = c->KV; aa.hd = c->hd; aa.chunk = sc.attn_chunk; aa.n_chunks = sc.attn_nch;
+    aa.T = T; aa.H = c->H; aa.KV = c->KV; aa.hd = c->hd; aa.split_keys = sc.attn_sk; aa.n_splits = sc.attn_ns;
     aa.part_acc = c->attn_acc; aa.part_ml = c->attn_ml; aa.out = c->att;
+    aa.qmap = c->attn_qmap; aa.kmap = aa.vmap = c->kv_map[which]; aa.counter = c->attn_cnt;
     size_t i0 = 0;
     if (c->timing.on) { i0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
     CK(launch_attention(aa, c->st));
@@ -364,7 +369,7 @@ static mg_status forward(mg_ctx* c, int T, const int32_t* slot, const int32_t* p
     // residual + the NEXT norm (next layer's attn_norm, or the final norm)
     const uint16_t* wn = l + 1 < c->L ? c->layers[l + 1].attn_norm : c->final_norm;
     CK(launch_residual_norm(c->x, c->part, sc.down.ps(), T, c->d, wn, eps, c->xn, c->st));
-    c->launches += 6;
+    c->launches += 5;
   }
   return MG_OK;
 }
@@ -469,7 +474,7 @@ static mg_status run_det(mg_ctx* c, int M, const std::vector<int>& last_host, in
     Sched sc = sched_det(c, T, max_ctx_hint);
     int r1 = r0;
     while (r1 < n_last && last_host[r1] < c0 + T) ++r1;
-    mg_status r = graphed(c, std::make_tuple(1, T, sc.attn_nch, c0, r0, r1), [&]() -> mg_status {
+    mg_status r = graphed(c, std::make_tuple(1, T, sc.attn_ns, c0, r0, r1), [&]() -> mg_status {
       mg_status rr = forward(c, T, c->cu_slot + c0, c->cu_pos + c0, c->cu_tok + c0, c->cu_nk + c0, 1, sc);
       if (rr) return rr;
       if (r1 > r0) {
@@ -591,11 +596,20 @@ mg_status mg_init(const mg_config* cfg, const mg_buffers* bufs, void* stream, mg
     for (Weight* w : {&l.qkv, &l.o, &l.gu, &l.down})
       if (!make_tmap_w_tiled(&w->map, w->ptr, w->K, w->N)) return die("cuTensorMapEncodeTiled failed (weights)");
   if (!make_tmap_w_tiled(&c->lm.map, c->lm.ptr, c->lm.K, c->lm.N)) return die("cuTensorMapEncodeTiled failed (lm)");
+  // attention: Q tiles of 16 heads, K/V blocks of 16 keys (AttnArgs)
+  const int64_t slabs = (int64_t)c->L * c->n_pages * 2 * c->KV;
+  if (!make_tmap_3d(&c->attn_qmap, c->q, c->hd, c->H, c->Tmax, 16) ||
+      !make_tmap_3d(&c->kv_map[0], c->kv_fast, c->hd, c->PS, slabs, 16) ||
+      !make_tmap_3d(&c->kv_map[1], c->kv_shadow, c->hd, c->PS, slabs, 16))
+    return die("cuTensorMapEncodeTiled failed (attention)");
 
   std::vector<float> cs, sn;
   init_rope(c->cfg, cs, sn);
   cudaError_t e;
+  // zeroed pools: a key block read past a sequence's end holds finite values
   if ((e = cudaMemsetAsync(bufs->workspace, 0, lay.workspace, c->st)) ||
+      (e = cudaMemsetAsync(bufs->kv_fast, 0, lay.kv, c->st)) ||
+      (e = cudaMemsetAsync(bufs->kv_shadow, 0, lay.kv, c->st)) ||
       (e = cudaMemcpyAsync(c->rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, c->st)) ||
       (e = cudaMemcpyAsync(c->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice, c->st)))
     return die(cudaGetErrorString(e));
@@ -707,9 +721,9 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
       c->launches++;
     }
   }
-  // 2. fast path (one CUDA graph per (B, attention chunks))
+  // 2. fast path (one CUDA graph per (B, attention splits))
   Sched fs = sched_fast(c, B, max_ctx);
-  mg_status r = graphed(c, std::make_tuple(0, B, fs.attn_nch, 0, 0, 0), [&]() -> mg_status {
+  mg_status r = graphed(c, std::make_tuple(0, B, fs.attn_ns, fs.attn_sk, 0, 0), [&]() -> mg_status {
     CK(launch_prepare(c->slots_d, B, c->pos_d, c->hist_d, c->cfg.max_seq + 1, c->f_slot, c->f_pos, c->f_tok,
                       c->f_nk, c->st));
     c->launches++;
@@ -934,7 +948,7 @@ mg_status mgd_schedule(mg_ctx* c, int32_t T, int32_t det, int32_t max_ctx, int32
   Sched s = det ? sched_det(c, T, max_ctx) : sched_fast(c, T, max_ctx);
   auto sp = [](const OpSched& x) { return x.G > 0 ? -x.G : x.splits; };  // < 0: stream-K over -v CTAs
   o[0] = sp(s.qkv); o[1] = sp(s.o); o[2] = sp(s.gu); o[3] = sp(s.down); o[4] = sp(s.lm);
-  o[5] = s.attn_chunk; o[6] = s.qkv.impl; o[7] = s.qkv.mma_n;
+  o[5] = -s.attn_sk; o[6] = s.qkv.impl; o[7] = s.qkv.mma_n;
   return MG_OK;
 }
 

@@ -25,7 +25,7 @@ struct OpSched {
 };
 struct Sched {
   OpSched qkv, o, gu, down, lm;
-  int attn_chunk, attn_nch;
+  int attn_sk, attn_ns;  // attention: keys per split, grid splits
 };
 
 struct Weight {
@@ -63,7 +63,6 @@ struct mg_ctx {
   int Tmax;   // activation rows
   int PS, max_pages, n_pages;
   int nb_top2;
-  int nch_max;
 
   // weights
   uint16_t *embed, *final_norm;
@@ -76,6 +75,8 @@ struct mg_ctx {
   // workspace
   uint16_t *x, *xn, *q, *att, *a, *xg, *xgn;
   float *part, *logits, *attn_acc, *attn_ml, *top2_part;
+  int32_t* attn_cnt;                     // [Tmax][KV] chunk-arrival counters
+  CUtensorMap attn_qmap, kv_map[2];      // TMA maps: q [Tmax][H][hd]; pools (fast, shadow)
   float *rope_cos, *rope_sin;
   size_t part_elems;
   // device state

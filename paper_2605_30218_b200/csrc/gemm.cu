@@ -143,6 +143,9 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = g.K / C::BK;
   long long* trace = ((g.dbg & 1024) && blockIdx.x == 0) ? reinterpret_cast<long long*>(g.out) : nullptr;
+  // dbg 2048: per-CTA globaltimer stamps [entry, first stage landed, last MMA issued, exit]
+  long long* ctr = (g.dbg & 2048) ? reinterpret_cast<long long*>(g.out) + blockIdx.x * 4 : nullptr;
+  if (ctr && threadIdx.x == 0) ctr[0] = (long long)globaltimer();
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&mapW);
@@ -223,6 +226,7 @@ __global__ void __launch_bounds__(192, 1)
         tc_fence_after();
         if (lane == 0) {
           if (trace && it < 256) trace[it * 4 + 1] = clock64();
+          if (ctr && it == 0) ctr[1] = (long long)globaltimer();
           // descriptor of (stage st, box i, k-step kk) = base + byte offset / 16
           const uint64_t a_st = a_desc0 + (uint64_t)((st * C::A_BYTES) >> 4);
           const uint64_t b_st = b_desc0 + (uint64_t)((st * C::B_BYTES) >> 4);
@@ -248,6 +252,7 @@ __global__ void __launch_bounds__(192, 1)
       if (lane == 0) tc_commit(&tfull[buf]);  // accumulator complete
       __syncwarp();
     }
+    if (ctr && lane == 0) ctr[2] = (long long)globaltimer();
   } else {  // ---- epilogue warps 2..5: TMEM lanes 32*(warp%4) ..
     griddep_wait();
     const int q = warp & 3;
@@ -288,6 +293,7 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     tc_dealloc(tmem, C::TMEM_COLS);
   }
+  if (ctr && threadIdx.x == 0) ctr[3] = (long long)globaltimer();
 }
 
 // ------------------------------------------------------------------ CUDA-core
@@ -354,6 +360,20 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, int inner_k, int rows, int b
   cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// 3-D bf16 tensor [d2][d1][d0] (d0 innermost, d0 % 64 == 0): box 64 x box1 x 1,
+// 128B swizzle -- attention's Q tiles and K/V blocks
+bool make_tmap_3d(CUtensorMap* m, const void* base, int d0, int64_t d1, int64_t d2, int box1) {
+  if (!get_encode() || d0 % 64 || d1 < 1 || d2 < 1 || d2 > INT32_MAX || d1 > INT32_MAX) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+  cuuint64_t strides[2] = {(cuuint64_t)d0 * 2, (cuuint64_t)d0 * 2 * (cuuint64_t)d1};
+  cuuint32_t box[3] = {64, (cuuint32_t)box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;

@@ -96,7 +96,6 @@ cudaError_t launch_epi_residual(const uint16_t* x, const float* part, PartSpec p
 // x <- bf16(x + sum_s part[s]); xn <- RMSNorm(x, w) (xn nullable)
 cudaError_t launch_residual_norm(uint16_t* x, const float* part, PartSpec ps, int T, int d, const uint16_t* w,
                                  float eps, uint16_t* xn, cudaStream_t st);
-int attn_max_chunk();
 cudaError_t launch_epi_swiglu(const float* part, PartSpec ps, int T, int F, uint16_t* out, cudaStream_t st);
 cudaError_t launch_gather_rows(const uint16_t* src, const int32_t* rows, int n, int d, uint16_t* dst,
                                cudaStream_t st);
@@ -104,7 +103,12 @@ cudaError_t launch_gather_rows(const uint16_t* src, const int32_t* rows, int n, 
 // ---- attention (a4)
 // Keys of token t: positions 0..n_keys(t)-1 of request slot(t) in the paged
 // cache (or dense K/V [T][KV][key_stride][hd] when cache == nullptr).
+// Q and K/V are read by TMA through 3-D maps (make_tmap_3d, box 64 x 16 x 1):
+//   qmap  over q        [T'][H][hd]                     (T' >= T rows allocated)
+//   kmap  paged: over the pool [L*n_pages*2*KV][PS][hd] (slab = ((l*n_pages+page)*2+kvsel)*KV+kvh)
+//         dense: over Kd [T*KV][key_stride][hd];  vmap: the same pool (paged) or Vd
 struct AttnArgs {
+  CUtensorMap qmap, kmap, vmap;
   const uint16_t* q;      // [T][H*hd]
   CacheView cache;        // paged view (engine), valid when paged != 0
   int32_t paged;
@@ -113,11 +117,15 @@ struct AttnArgs {
   const uint16_t* Kd;     // dense (debug)
   const uint16_t* Vd;
   int32_t key_stride;
-  int32_t T, H, KV, hd, chunk, n_chunks;
-  float* part_acc;        // [T][H][n_chunks][hd]
-  float* part_ml;         // [T][H][n_chunks][2]
+  int32_t T, H, KV, hd;
+  int32_t split_keys;     // keys per split (multiple of 64); token t has ceil(n_keys/split_keys) splits
+  int32_t n_splits;       // grid splits (>= the max over tokens)
+  float* part_acc;        // [T][H][n_splits][hd]  split partials (tokens with > 1 split)
+  float* part_ml;         // [T][H][n_splits][2]
+  int32_t* counter;       // [T][KV] arrival counters, zero between launches
   uint16_t* out;          // [T][H*hd]
 };
+bool make_tmap_3d(CUtensorMap* m, const void* base, int d0, int64_t d1, int64_t d2, int box1);
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st);
 
 // ---- top-2, gate, catch-up, commit (a8-a11)

@@ -323,15 +323,20 @@ def test_wide_shallow_parity(orc, torch):
         st = orc.State(m, B, 32)
         det = orc.det_sched()
         y0 = [eng.prefill(i, p) for i, p in enumerate(prompts)]
-        y0o = [st.prefill(i, p, det) for i, p in enumerate(prompts)]
-        assert sum(a == b for a, b in zip(y0, y0o)) >= B - 1
+        pre = [st.prefill(i, p, det, want_logits=True) for i, p in enumerate(prompts)]
+        # a first token may differ only inside the argmax-ambiguity band; such a
+        # row then consumes a different input token and is left out below
+        same = np.array([a == b for a, (b, _) in zip(y0, pre)])
+        for i in np.nonzero(~same)[0]:
+            assert float(orc.top2(pre[i][1])["g"][0]) <= BAND, i
+        assert same.sum() >= B - 2
         out = torch.empty(B, dtype=torch.int32, device="cuda")
         for _ in range(3):
             eng.step(list(range(B)), None, 0.0, out)
             o = out.cpu().numpy()
             r = st.step(np.arange(B), np.zeros(B, np.uint8), 0.0, orc.fast_sched(B), det, forced_out=o,
                         forced_kind=np.zeros(B, np.uint8), want_logits=True)
-            _check_logit_err(np.abs(cap.cpu().numpy() - r["logits"]))
+            _check_logit_err(np.abs(cap.cpu().numpy() - r["logits"])[same])
         eng.close()
         st.close()
     p = inputs.prompts(1, 9, shp["vocab"], seed=777)[0]

@@ -178,19 +178,26 @@ def test_qkv_epilogue_bit_exact(orc, K, H, KV, hd, bias, S):
 
 
 # ------------------------------------------------------------------ a4
-@pytest.mark.parametrize("H,KV,hd,chunk", [(4, 4, 64, 64), (4, 2, 64, 128), (32, 8, 128, 256), (40, 8, 128, 64),
-                                           (28, 4, 128, 128), (32, 8, 128, 64), (64, 4, 128, 128)])
-def test_attention(orc, K, H, KV, hd, chunk):
-    rng = np.random.default_rng(H * hd + chunk)
-    T, stride = 4, 700
-    n_keys = np.array([1, 37, 513, 700], np.int32)
+# split_keys: 64 / 128 -> many splits (last-CTA combine); 512 -> 1-2 splits;
+# 4096 with 2600 keys -> one split of 163 blocks (> 32 per warp: the
+# page-coordinate batches of the ring refill)
+@pytest.mark.parametrize("H,KV,hd,sk,stride,nk", [
+    (4, 4, 64, 64, 700, (1, 37, 513, 700)), (4, 2, 64, 128, 700, (1, 37, 513, 700)),
+    (32, 8, 128, 512, 700, (1, 37, 513, 700)), (40, 8, 128, 64, 700, (1, 37, 513, 700)),
+    (28, 4, 128, 128, 700, (1, 37, 513, 700)), (32, 8, 128, 64, 700, (16, 64, 65, 700)),
+    (64, 4, 128, 128, 700, (1, 37, 513, 700)), (32, 8, 128, 4096, 2600, (2100, 2600)),
+    (8, 8, 64, 4096, 2600, (17, 2600))])
+def test_attention(orc, K, H, KV, hd, sk, stride, nk):
+    rng = np.random.default_rng(H * hd + sk + stride)
+    n_keys = np.array(nk, np.int32)
+    T = len(nk)
     q = _rand(orc, rng, (T, H, hd))
     Kc = _rand(orc, rng, (T, KV, stride, hd))
     Vc = _rand(orc, rng, (T, KV, stride, hd))
-    o = K.attention(q, Kc, Vc, n_keys, chunk)
+    o = K.attention(q, Kc, Vc, n_keys, sk)
     vmax = float(np.abs(_bf(orc, Vc)).max())
     for t in range(T):
-        ref = orc.attention(q[t], Kc[t], Vc[t], int(n_keys[t]), chunk, 1)
+        ref = orc.attention(q[t], Kc[t], Vc[t], int(n_keys[t]), -sk, 1)   # the streamed form (A14)
         # 2 bf16 ulp, plus an absolute fp32-reordering slack for outputs that
         # cancel to ~0 (weighted means of values of size vmax)
         ok = (_ulps(orc, o[t], ref) <= 2.0) | (np.abs(_bf(orc, o[t]) - _bf(orc, ref)) <= 1e-5 * vmax)

@@ -260,9 +260,12 @@ def _attn_fp64(q, K, V, n):
     return out
 
 
-@pytest.mark.parametrize("n,chunk,splits", [(1, 0, 1), (37, 0, 1), (37, 16, 1), (200, 0, 7), (200, 64, 1)])
+# chunk < 0: the streamed form (4 round-robin block streams per split of -chunk keys)
+@pytest.mark.parametrize("n,chunk,splits", [(1, 0, 1), (37, 0, 1), (37, 16, 1), (200, 0, 7), (200, 64, 1),
+                                            (1, -64, 1), (37, -64, 1), (200, -64, 1), (250, -512, 1),
+                                            (77, -16, 1)])
 def test_attention_fp64(orc, n, chunk, splits):
-    rng = np.random.default_rng(n + chunk + splits)
+    rng = np.random.default_rng(n + abs(chunk) + splits)
     H, KVh, hd, stride = 8, 2, 64, 256
     q = _rand_bf16(orc, rng, (H, hd))
     K = _rand_bf16(orc, rng, (KVh, stride, hd))
@@ -273,18 +276,19 @@ def test_attention_fp64(orc, n, chunk, splits):
     assert np.all(np.abs(o - ref) <= np.abs(ref) * 2 ** -7 + 1e-5 * np.abs(f(V)).max())
 
 
-def test_attention_special_cases(orc):
+@pytest.mark.parametrize("chunk", [0, -64, -16])
+def test_attention_special_cases(orc, chunk):
     rng = np.random.default_rng(9)
     H, KVh, hd = 4, 4, 64
     q = _rand_bf16(orc, rng, (H, hd))
     K = _rand_bf16(orc, rng, (KVh, 8, hd))
     V = _rand_bf16(orc, rng, (KVh, 8, hd))
     # one key: softmax weight exactly 1 -> o == v
-    o = orc.attention(q, K, V, 1).reshape(H, hd)
+    o = orc.attention(q, K, V, 1, chunk).reshape(H, hd)
     assert np.array_equal(o, V[:, 0, :])
     # identical keys: uniform weights -> o == mean of the values (fp64, 1 ulp)
     K2 = np.repeat(K[:, :1, :], 8, axis=1)
-    o2 = orc.bf16_to_f32(orc.attention(q, K2, V, 8)).reshape(H, hd).astype(np.float64)
+    o2 = orc.bf16_to_f32(orc.attention(q, K2, V, 8, chunk)).reshape(H, hd).astype(np.float64)
     ref = orc.bf16_to_f32(V).astype(np.float64).mean(1)
     assert np.all(np.abs(o2 - ref) <= np.abs(ref) * 2 ** -7 + 1e-6)
 
