@@ -106,7 +106,7 @@ def run_gpu(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2605_30218_b200 import inputs, metrics
+    from paper_2605_30218_b200 import inputs, metrics, sharding
     from paper_2605_30218_b200.engine import Engine
 
     ws, rank, local = _dist()
@@ -121,7 +121,7 @@ def run_gpu(args):
     max_seq = ctx0 + W + K + 2
     eng = Engine(shp, max_batch=B, max_slots=B, max_seq=max_seq, page_size=64)
     # requests of this rank: global ids rank*B .. rank*B + B-1 (request i -> rank i // B)
-    prompts = inputs.prompts(B, ctx0, shp["vocab"], seed=7 + rank * B)
+    prompts = inputs.prompts(B, ctx0, shp["vocab"], seed=7 + sharding.rank_requests(rank, ws, B)[0])
     out = torch.empty(B, dtype=torch.int32, device="cuda")
     kind = torch.empty(B, dtype=torch.uint8, device="cuda")
     stream = eng.stream
@@ -221,13 +221,7 @@ def run_gpu(args):
     do = det("mg_other", "ao_other", prot_all if other == "all" else prot_one) if "mg_other" in res else (0, 0)
     vec += [*dh, *do]
     times = [res[a]["ms"] for a in arms] + [e2e_ms]
-    if ws > 1:
-        tv = torch.tensor(vec, dtype=torch.int64, device="cuda")
-        dist.all_reduce(tv, op=dist.ReduceOp.SUM)
-        vec = tv.tolist()
-        tt = torch.tensor(times, dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        times = tt.tolist()
+    vec, times = sharding.aggregate(vec, times, device="cuda")
     if rank != 0:
         if ws > 1:
             dist.destroy_process_group()

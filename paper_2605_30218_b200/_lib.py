@@ -11,7 +11,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libmargingate.so")
+# MG_LIB_PATH: another in-tree build of the same library (A/B timing scripts only)
+LIB_PATH = os.environ.get("MG_LIB_PATH") or os.path.join(_HERE, "lib", "libmargingate.so")
 _lock = threading.Lock()
 _lib = None
 

@@ -25,7 +25,9 @@
 // Data movement: TMA only.  Each warp owns a ring of R stages (K block + V
 // block, box 64 dims x 16 keys, 128B swizzle -> conflict-free ldmatrix) that
 // its lane 0 refills as soon as the warp has consumed a stage; warp 0 loads
-// the Q tile once.  Page-table lookups for 32 blocks at a time are done by the
+// the Q tile once.  On the fast path (prewait) the first blocks, which hold
+// only keys of earlier steps, are requested before griddepcontrol.wait, so
+// their latency overlaps the tail of the QKV epilogue.  Page-table lookups for 32 blocks at a time are done by the
 // 32 lanes in parallel and shuffled to lane 0 at issue time.
 #include <cstdlib>
 
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
     fence_mbar_init();
   }
   __syncthreads();
-  griddep();
+  if (!a.prewait) griddep();
   const int n = a.n_keys[t];
   const int lo = sp * a.split_keys;
   if (lo >= n) return;
@@ -139,13 +141,23 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
         tma_load_3d(st + C::BLK + h * 2048, &a.vmap, &full[s], 64 * h, row, sl + vsl);
     }
   };
+  coords(0);
+  int issued = 0;
+  if (a.prewait) {
+    // PDL: blocks whose keys all precede this step's appended column (n - 1)
+    // were written by earlier steps -- fetched before griddepcontrol.wait
+    for (; issued < R && issued < nbw; ++issued) {
+      if (lo + 16 * (warp + 4 * issued) + 16 > n - 1) break;
+      issue(issued);
+    }
+    griddep();
+  }
   if (warp == 0 && lane == 0) {
     mbar_expect_tx(&bars[0], C::BLK);
 #pragma unroll
     for (int h = 0; h < C::HALVES; ++h) tma_load_3d(sm + C::Q_OFF + h * 2048, &a.qmap, &bars[0], 64 * h, kvh * G, t);
   }
-  coords(0);
-  for (int i = 0; i < R && i < nbw; ++i) issue(i);
+  for (int i = issued; i < R && i < nbw; ++i) issue(i);
 
   const int rr = lane & 7, mi = lane >> 3;
   const int r0 = lane >> 2, r1 = r0 + 8, cc = 2 * (lane & 3);

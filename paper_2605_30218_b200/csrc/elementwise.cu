@@ -176,44 +176,63 @@ __device__ __forceinline__ void sum8_pieces(const float* __restrict__ part, int 
 }
 
 constexpr int kResThreads = 512;
+constexpr int kResMaxV = 2;  // 8-feature vectors per thread: d <= 2 * 512 * 8
 
+// PDL: the residual row (last written >= 2 kernels earlier) and the gains do
+// not depend on the immediately preceding kernel, so they are loaded before
+// griddepcontrol.wait; only the GEMM partials are read after it.
 __global__ void __launch_bounds__(kResThreads) k_residual_norm(uint16_t* __restrict__ x, const float* __restrict__ part,
                                                                PartSpec ps, int T, int d,
                                                                const uint16_t* __restrict__ w, float eps,
                                                                uint16_t* __restrict__ xn) {
   __shared__ float red[kResThreads / 32];
   __shared__ float s_inv;
-  extern __shared__ uint4 hrow[];  // the new residual row, d/8 vectors
-  griddep();
   const int t = blockIdx.x;
   const size_t stride = (size_t)T * d;
   uint4* xv = reinterpret_cast<uint4*>(x + (size_t)t * d);
+  const uint4* wv = reinterpret_cast<const uint4*>(w);
   const int nv = d / 8;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < nv; i += kResThreads) {
-    const uint4 v = xv[i];
-    const uint32_t u[4] = {v.x, v.y, v.z, v.w};
-    float acc[8];
-    sum8_pieces(part, part_count(ps, i * 8), stride, (size_t)t * d + (size_t)i * 8, acc);  // one 128-feature tile
-    uint32_t r[4];
+  uint4 hr[kResMaxV], wr[kResMaxV];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      r[j] = pack_bf2(__fadd_rn(lo_bf(u[j]), acc[2 * j]), __fadd_rn(hi_bf(u[j]), acc[2 * j + 1]));
-    const uint4 h = make_uint4(r[0], r[1], r[2], r[3]);
-    hrow[i] = h;
-    xv[i] = h;
-    ss = ss8(h, ss);
+  for (int j = 0; j < kResMaxV; ++j) {
+    const int i = threadIdx.x + j * kResThreads;
+    if (i < nv) {
+      hr[j] = __ldcg(xv + i);
+      if (xn) wr[j] = __ldg(wv + i);
+    }
+  }
+  griddep();
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < kResMaxV; ++j) {
+    const int i = threadIdx.x + j * kResThreads;
+    if (i < nv) {
+      const uint32_t u[4] = {hr[j].x, hr[j].y, hr[j].z, hr[j].w};
+      float acc[8];
+      sum8_pieces(part, part_count(ps, i * 8), stride, (size_t)t * d + (size_t)i * 8, acc);  // one 128-feature tile
+      uint32_t r[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        r[q] = pack_bf2(__fadd_rn(lo_bf(u[q]), acc[2 * q]), __fadd_rn(hi_bf(u[q]), acc[2 * q + 1]));
+      hr[j] = make_uint4(r[0], r[1], r[2], r[3]);
+      xv[i] = hr[j];
+      ss = ss8(hr[j], ss);
+    }
   }
   const float inv = block_inv_rms(ss, d, eps, red, &s_inv);
   if (!xn) return;
-  const uint4* wv = reinterpret_cast<const uint4*>(w);
   uint4* ov = reinterpret_cast<uint4*>(xn + (size_t)t * d);
-  for (int i = threadIdx.x; i < nv; i += kResThreads) ov[i] = norm8(hrow[i], __ldg(wv + i), inv);
+#pragma unroll
+  for (int j = 0; j < kResMaxV; ++j) {
+    const int i = threadIdx.x + j * kResThreads;
+    if (i < nv) ov[i] = norm8(hr[j], wr[j], inv);
+  }
 }
 
 cudaError_t launch_residual_norm(uint16_t* x, const float* part, PartSpec ps, int T, int d, const uint16_t* w,
                                  float eps, uint16_t* xn, cudaStream_t st) {
-  return launch_k(k_residual_norm, dim3(T), dim3(kResThreads), (size_t)d * 2, st, x, part, ps, T, d, w, eps, xn);
+  if (d % 8 || d > kResMaxV * kResThreads * 8) return cudaErrorInvalidValue;
+  return launch_k(k_residual_norm, dim3(T), dim3(kResThreads), 0, st, x, part, ps, T, d, w, eps, xn);
 }
 
 // ------------------------------------------------------------------ a3 epilogue
@@ -229,39 +248,45 @@ __global__ void k_epi_qkv(const float* __restrict__ part, PartSpec ps, const uin
                           const float* __restrict__ rcos, const float* __restrict__ rsin, uint16_t* __restrict__ q,
                           CacheView cache, bool paged, const int32_t* __restrict__ slot, uint16_t* __restrict__ kd,
                           uint16_t* __restrict__ vd) {
-  griddep();
+  // PDL: positions, bias, RoPE factors and the cache slot do not depend on
+  // the preceding kernel (the QKV GEMM) -- gathered before griddepcontrol.wait
   const int t = blockIdx.x, h = blockIdx.y, i = threadIdx.x, h2 = hd / 2;
   const int NQKV = (H + 2 * KV) * hd;
   const size_t stride = (size_t)T * NQKV;
   const int f1 = h * hd + i, f2 = f1 + h2;
+  const int p = pos[t];
+  float ba = 0.f, bb = 0.f, c = 1.f, sn = 0.f;
+  if (bias) {
+    ba = bf2f(bias[f1]);
+    bb = bf2f(bias[f2]);
+  }
+  if (h < H + KV) {
+    c = rcos[(size_t)p * h2 + i];
+    sn = rsin[(size_t)p * h2 + i];
+  }
+  uint16_t* dst;
+  if (h < H) {
+    dst = q + (size_t)t * H * hd + h * hd;
+  } else {
+    const int kvsel = h < H + KV ? 0 : 1;
+    const int kh = h - H - kvsel * KV;
+    dst = paged ? cache_ptr(cache, slot[t], p, kvsel, kh)  // tentative append of column p
+                : (kvsel ? vd : kd) + (size_t)t * KV * hd + kh * hd;
+  }
+  griddep();
   float a = sum_splits(part, part_count(ps, f1), stride, (size_t)t * NQKV + f1);
   float b = sum_splits(part, part_count(ps, f2), stride, (size_t)t * NQKV + f2);
   if (bias) {
-    a = __fadd_rn(a, bf2f(bias[f1]));
-    b = __fadd_rn(b, bf2f(bias[f2]));
+    a = __fadd_rn(a, ba);
+    b = __fadd_rn(b, bb);
   }
-  const int p = pos[t];
   uint16_t oa, ob;
   if (h < H + KV) {  // RoPE on q and k
-    const float c = rcos[(size_t)p * h2 + i], s = rsin[(size_t)p * h2 + i];
-    oa = f2bf(__fsub_rn(__fmul_rn(a, c), __fmul_rn(b, s)));
-    ob = f2bf(__fadd_rn(__fmul_rn(b, c), __fmul_rn(a, s)));
+    oa = f2bf(__fsub_rn(__fmul_rn(a, c), __fmul_rn(b, sn)));
+    ob = f2bf(__fadd_rn(__fmul_rn(b, c), __fmul_rn(a, sn)));
   } else {
     oa = f2bf(a);
     ob = f2bf(b);
-  }
-  if (h < H) {
-    q[(size_t)t * H * hd + h * hd + i] = oa;
-    q[(size_t)t * H * hd + h * hd + i + h2] = ob;
-    return;
-  }
-  const int kvsel = h < H + KV ? 0 : 1;
-  const int kh = h - H - kvsel * KV;
-  uint16_t* dst;
-  if (paged) {
-    dst = cache_ptr(cache, slot[t], p, kvsel, kh);  // tentative append of column p
-  } else {
-    dst = (kvsel ? vd : kd) + (size_t)t * KV * hd + kh * hd;
   }
   dst[i] = oa;
   dst[i + h2] = ob;

@@ -60,6 +60,7 @@ bool valid_cfg(const mg_config* c, std::string* why) {
   if (((c->n_heads + 2 * c->n_kv_heads) * c->head_dim) % 128) return bad("(H+2KV)*hd must be a multiple of 128");
   if ((c->n_heads * c->head_dim) % 64) return bad("H*hd must be a multiple of 64");
   if (c->d_model % 128) return bad("d_model must be a multiple of 128");
+  if (c->d_model > 8192) return bad("d_model > 8192 unsupported (k_residual_norm row in registers)");
   if (c->vocab % 128) return bad("vocab must be a multiple of 128");
   if (c->max_batch < 1 || c->max_batch > 256) return bad("max_batch must be in [1, 256]");
   if (c->max_slots < c->max_batch) return bad("max_slots < max_batch");
@@ -354,6 +355,7 @@ static mg_status forward(mg_ctx* c, int T, const int32_t* slot, const int32_t* p
     aa.T = T; aa.H = c->H; aa.KV = c->KV; aa.hd = c->hd; aa.split_keys = sc.attn_sk; aa.n_splits = sc.attn_ns;
     aa.part_acc = c->attn_acc; aa.part_ml = c->attn_ml; aa.out = c->att;
     aa.qmap = c->attn_qmap; aa.kmap = aa.vmap = c->kv_map[which]; aa.counter = c->attn_cnt;
+    aa.prewait = which == 0;  // fast path: each token appended only its own column
     size_t i0 = 0;
     if (c->timing.on) { i0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
     CK(launch_attention(aa, c->st));

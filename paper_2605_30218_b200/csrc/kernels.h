@@ -124,6 +124,8 @@ struct AttnArgs {
   float* part_ml;         // [T][H][n_splits][2]
   int32_t* counter;       // [T][KV] arrival counters, zero between launches
   uint16_t* out;          // [T][H*hd]
+  int32_t prewait;        // 1: keys < n_keys-1 predate the previous kernel (fast path: one new column
+                          //    per token) and may be read before griddepcontrol.wait
 };
 bool make_tmap_3d(CUtensorMap* m, const void* base, int d0, int64_t d1, int64_t d2, int box1);
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st);
