@@ -14,9 +14,12 @@
 
 using namespace mg;
 
+#ifndef SK_MAX
+#define SK_MAX 148
+#endif
 static int sk_G(int N, int K) {
   const int W = (N / 128) * (K / 64);
-  return std::max(1, std::min(W / 4, 148));
+  return std::max(1, std::min(W / 4, SK_MAX));
 }
 
 int main(int argc, char** argv) {
@@ -51,7 +54,7 @@ int main(int argc, char** argv) {
   for (int s = 0; s < 5; ++s) {
     const int N = shapes[s][0], K = shapes[s][1];
     const double bytes = (double)N * K * 2;
-    for (int G : {sk_G(N, K), 74, 296}) {
+    for (int G : {sk_G(N, K)}) {
       if (s == 4 && G != sk_G(N, K)) continue;
       if (G > (N / 128) * (K / 64)) continue;
       g_gemm_dbg = 0;
@@ -75,17 +78,17 @@ int main(int argc, char** argv) {
       }
       // per-CTA timeline of one isolated launch (stores skipped: out holds the stamps)
       g_gemm_dbg = 2048 | 2;
-      cudaMemset(out, 0, 148 * 4 * 8);
+      cudaMemset(out, 0, 296 * 4 * 8);
       launch(s, G);
       cudaDeviceSynchronize();
-      std::vector<long long> tr(148 * 4);
+      std::vector<long long> tr(296 * 4);
       cudaMemcpy(tr.data(), out, tr.size() * 8, cudaMemcpyDeviceToHost);
       int n = 0;
       long long t0 = 1LL << 62;
-      for (int c = 0; c < 148; ++c)
+      for (int c = 0; c < 296; ++c)
         if (tr[c * 4]) { t0 = std::min(t0, tr[c * 4]); ++n; }
       std::vector<double> ent, first, mma, ex;
-      for (int c = 0; c < 148; ++c)
+      for (int c = 0; c < 296; ++c)
         if (tr[c * 4]) {
           ent.push_back((tr[c * 4] - t0) * 1e-3);
           first.push_back((tr[c * 4 + 1] - tr[c * 4]) * 1e-3);

@@ -1,0 +1,60 @@
+"""Kernel timeline of pipelined decode steps via torch.profiler (CUPTI) -- diagnostic only.
+
+usage: python scripts/timeline.py [model] [B] [ctx] [tau] [steps] > summary
+Prints per kernel class: count, mean duration, and the mean gap between the
+end of the previous kernel and the start of this one (the pipeline bubble).
+"""
+import collections
+import json
+import os
+import sys
+import tempfile
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_30218_b200 import inputs  # noqa: E402
+from paper_2605_30218_b200.engine import Engine  # noqa: E402
+
+model = sys.argv[1] if len(sys.argv) > 1 else "llama8b"
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+ctx = int(sys.argv[3]) if len(sys.argv) > 3 else 384
+tau = float(sys.argv[4]) if len(sys.argv) > 4 else 0.0
+steps = int(sys.argv[5]) if len(sys.argv) > 5 else 3
+shp = inputs.shape(model)
+eng = Engine(shp, max_batch=B, max_seq=ctx + 64, page_size=64)
+for i, p in enumerate(inputs.prompts(B, ctx, shp["vocab"])):
+    eng.prefill(i, p)
+out = torch.empty(B, dtype=torch.int32, device="cuda")
+rows = list(range(B))
+for _ in range(6):
+    eng.step(rows, None, tau, out)
+torch.cuda.synchronize()
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(steps):
+        eng.step(rows, None, tau, out)
+    torch.cuda.synchronize()
+fn = os.path.join(tempfile.mkdtemp(), "t.json")
+prof.export_chrome_trace(fn)
+ev = json.load(open(fn))["traceEvents"]
+ks = sorted([e for e in ev if e.get("cat") == "kernel"], key=lambda e: e["ts"])
+print(f"{len(ks)} kernels in {steps} steps; span {(ks[-1]['ts'] + ks[-1]['dur'] - ks[0]['ts']) / steps:.1f} us/step")
+# critical-path accounting: each kernel is charged end(k) - end(k-1), the time
+# it added to the stream (PDL lets a kernel START before its predecessor ends,
+# so start-based durations overlap)
+agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+prev_end = None
+for e in ks:
+    n = e["name"].split("(")[0].replace("void ", "")[:34]
+    end = e["ts"] + e["dur"]
+    a = agg[n]
+    a[0] += 1
+    a[1] += e["dur"]
+    if prev_end is not None:
+        a[2] += end - prev_end
+    prev_end = max(prev_end or 0, end)
+for n, a in sorted(agg.items(), key=lambda x: -x[1][2]):
+    print(f"{n:36s} n={a[0]:5d} start-to-end {a[1] / a[0]:8.2f} us  end-to-end {a[2] / a[0]:7.2f} us  "
+          f"= {a[2] / steps:8.1f} us/step")
+print(f"sum end-to-end {sum(a[2] for a in agg.values()) / steps:.1f} us/step")
