@@ -99,6 +99,12 @@ mg_status mgd_launch_count(mg_ctx* ctx, uint64_t* out_host);
 mg_status mgd_set_timing(mg_ctx* ctx, int32_t on);
 mg_status mgd_timing(mg_ctx* ctx, double* out8_host);
 
+/* Diagnostics of the persistent layer chain: from the next step on, the chain
+ * launch of `layer` records per-CTA globaltimer stamps (chain.h
+ * kChainTraceWords per CTA).  *words receives the buffer length; out_host
+ * (nullable) receives the stamps of the last traced launch.  layer -2: off. */
+mg_status mgd_chain_trace(mg_ctx* ctx, int32_t layer, unsigned long long* out_host, int32_t* words);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,8 +51,12 @@ struct PartSpec {
 __host__ __device__ __forceinline__ int part_count(const PartSpec& p, int n) {
   if (p.G == 0) return p.S;
   const long long W = (long long)p.n_m * p.KB;
-  const long long m = n / 128;
-  return streamk_owner((m + 1) * p.KB - 1, W, p.G) - streamk_owner(m * p.KB, W, p.G) + 1;
+  const int m = n / 128;
+  if (W * (p.G + 1) < 2147483647LL) {  // the same formula in 32-bit arithmetic (hot in the epilogues)
+    const int w0 = m * p.KB, w1 = (m + 1) * p.KB - 1, Wi = (int)W;
+    return ((w1 + 1) * p.G - 1) / Wi - ((w0 + 1) * p.G - 1) / Wi + 1;
+  }
+  return streamk_owner((long long)(m + 1) * p.KB - 1, W, p.G) - streamk_owner((long long)m * p.KB, W, p.G) + 1;
 }
 
 // ------------------------------------------------------------------ PDL
@@ -78,6 +82,8 @@ MG_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluste
 // order this thread's generic-proxy shared-memory accesses before later
 // async-proxy (TMA) writes to the same buffer
 MG_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// the same for global memory: generic-proxy stores before later TMA reads
+MG_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 MG_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -130,6 +136,10 @@ MG_DEV void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, 
       "[%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+// bulk L2 prefetch of a contiguous global range (size a multiple of 16 B)
+MG_DEV void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 MG_DEV void tma_load_4d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3,
                              uint64_t policy) {

@@ -76,6 +76,11 @@ struct mg_ctx {
   uint16_t *x, *xn, *q, *att, *a, *xg, *xgn;
   float *part, *logits, *attn_acc, *attn_ml, *top2_part;
   int32_t* attn_cnt;                     // [Tmax][KV] chunk-arrival counters
+  uint32_t* chain_sync;                  // layer-chain grid barriers + epoch (chain.h)
+  bool use_chain = false;                // MG_CHAIN=1: persistent layer chain (A/B only; slower today)
+  unsigned long long* chain_trace = nullptr;  // diagnostics (mgd_chain_trace)
+  int chain_trace_layer = -2;
+  int chain_pf = 0;  // chain L2 run-ahead (k-blocks per CTA; measured harmful, off)
   CUtensorMap attn_qmap, kv_map[2];      // TMA maps: q [Tmax][H][hd]; pools (fast, shadow)
   float *rope_cos, *rope_sin;
   size_t part_elems;

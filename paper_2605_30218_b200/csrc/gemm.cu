@@ -32,16 +32,11 @@
 // choice): warp per output row, 128-bit weight loads, fp32 FMA, fixed
 // xor-shuffle tree.
 #include "common.cuh"
+#include "gemm_tc.cuh"
 #include "kernels.h"
 
-#ifndef MG_GEMM_SMEM_KB
-#define MG_GEMM_SMEM_KB 192  // smem ring budget per CTA
-#endif
-#ifndef MG_GEMM_NS_MAX
-#define MG_GEMM_NS_MAX 8
-#endif
-#ifndef MG_GEMM_KS
-#define MG_GEMM_KS 2
+#ifndef MG_EPI_WAIT
+#define MG_EPI_WAIT mbar_wait  // accumulator-ready wait of the epilogue poller
 #endif
 
 namespace mg {
@@ -49,87 +44,11 @@ namespace mg {
 int g_pdl = 1;
 int g_gemm_dbg = 0;  // microbenchmark knobs (scripts/gemm_bench.cu); always 0 in the library
 
-template <int TN>
-struct GemmTcCfg {
-  static constexpr int BM = 128, BK = 64;
-  static constexpr int KS = MG_GEMM_KS;      // 64-wide k-blocks per pipeline stage
-  static constexpr int A_BOX = BM * BK * 2;  // one TMA box (16 KB, contiguous in HBM)
-  static constexpr int B_BOX = TN * BK * 2;
-  static constexpr int A_BYTES = KS * A_BOX;
-  static constexpr int B_BYTES = KS * B_BOX;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int NS0 = (MG_GEMM_SMEM_KB * 1024) / STAGE;
-  static constexpr int NS = NS0 > MG_GEMM_NS_MAX ? MG_GEMM_NS_MAX : NS0;
-  static constexpr int ACC_COLS = TN < 32 ? 32 : TN;
-  static constexpr int TMEM_COLS = 2 * ACC_COLS;
-  static constexpr int THREADS = 192;
-  static constexpr int SMEM = 1024 + NS * STAGE + (2 * NS + 4) * 8 + 16;
-  static_assert(NS >= 2, "pipeline needs two stages");
-};
-
-struct GemmArgs {
-  int N, K, T, splits;
-  int n_m, n_t, units;
-  int G;    // > 0: stream-K over G virtual CTAs per token tile; 0: uniform split-K
-  int dbg;  // microbenchmark knobs (0 in the product): 1 skip MMAs, 2 skip stores, 1024 trace CTA 0
-  float* out;
-};
-
-// A piece = one contiguous k-block range of one 128-feature tile for one
-// token tile; its fp32 partial goes to out[slot].  Every role of the CTA
-// walks the same piece sequence.
-struct Piece {
-  int mt, kb0, kb1, slot, tt;
-};
-struct PieceIter {
-  int KB, n_m, n_t, S, G, units;
-  long long W, w, w1;
-  int v, i, tt, u;
-  __device__ explicit PieceIter(const GemmArgs& g, int KB_) {
-    KB = KB_; n_m = g.n_m; n_t = g.n_t; S = g.splits; G = g.G; units = g.units;
-    W = (long long)n_m * KB;
-    u = blockIdx.x;
-    v = (int)blockIdx.x - (int)gridDim.x;
-    w = w1 = 0;
-    i = tt = 0;
-  }
-  __device__ bool next(Piece& p) {
-    if (G == 0) {
-      if (u >= units) return false;
-      p.tt = u % n_t;
-      const int r = u / n_t;
-      p.slot = r % S;
-      p.mt = r / S;
-      p.kb0 = chunk_start(KB, S, p.slot);
-      p.kb1 = chunk_start(KB, S, p.slot + 1);
-      u += gridDim.x;
-      return true;
-    }
-    while (w >= w1) {
-      v += gridDim.x;
-      if (v >= G * n_t) return false;
-      tt = v / G;
-      i = v % G;
-      w = (long long)i * W / G;
-      w1 = (long long)(i + 1) * W / G;
-    }
-    p.tt = tt;
-    p.mt = (int)(w / KB);
-    p.kb0 = (int)(w % KB);
-    p.kb1 = (int)min((long long)KB, p.kb0 + (w1 - w));
-    p.slot = i - streamk_owner((long long)p.mt * KB, W, G);
-    w += p.kb1 - p.kb0;
-    return true;
-  }
-};
-
 template <int TN, bool MMA16>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, GemmArgs g) {
   using C = GemmTcCfg<TN>;
   constexpr int KS = C::KS;
-  constexpr int MN = MMA16 ? 16 : TN;  // instruction N
-  constexpr int NG = TN / MN;          // instructions per k-step
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -208,7 +127,6 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else if (warp == 1) {
     // ---- MMA issuer: warp-uniform loop, lane 0 issues tcgen05.mma / commit
-    constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MN >> 3) << 17) | ((128u >> 4) << 24);
     const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
     const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB));
     const bool do_mma = !(g.dbg & 1);
@@ -230,20 +148,7 @@ __global__ void __launch_bounds__(192, 1)
           // descriptor of (stage st, box i, k-step kk) = base + byte offset / 16
           const uint64_t a_st = a_desc0 + (uint64_t)((st * C::A_BYTES) >> 4);
           const uint64_t b_st = b_desc0 + (uint64_t)((st * C::B_BYTES) >> 4);
-#pragma unroll
-          for (int i = 0; i < KS; ++i) {
-            if (i < nk && do_mma) {
-#pragma unroll
-              for (int kk = 0; kk < C::BK / 16; ++kk) {
-                const uint64_t ad = a_st + (uint64_t)((i * C::A_BOX + kk * 32) >> 4);
-#pragma unroll
-                for (int gi = 0; gi < NG; ++gi) {
-                  const uint64_t bd = b_st + (uint64_t)((i * C::B_BOX + gi * MN * 128 + kk * 32) >> 4);
-                  tc_mma_bf16(dacc + (uint32_t)(gi * MN), ad, bd, idesc, (kb + i > pc.kb0 || kk > 0) ? 1u : 0u);
-                }
-              }
-            }
-          }
+          if (do_mma) issue_stage<TN, MMA16>(a_st, b_st, nk, dacc, kb == pc.kb0);
           tc_commit(&empty[st]);  // frees the smem stage when these MMAs retire
           if (trace && it < 256) trace[it * 4 + 2] = clock64();
         }
@@ -261,7 +166,7 @@ __global__ void __launch_bounds__(192, 1)
     for (; pi.next(pc); ++j) {
       const int buf = j & 1;
       // one thread polls the mbarrier; the other 127 sleep in a named barrier
-      if (warp == 2 && lane == 0) mbar_wait(&tfull[buf], (uint32_t)(j >> 1) & 1u);
+      if (warp == 2 && lane == 0) MG_EPI_WAIT(&tfull[buf], (uint32_t)(j >> 1) & 1u);
       asm volatile("bar.sync 1, 128;" ::: "memory");
       tc_fence_after();
       const int n = pc.mt * C::BM + q * 32 + lane;

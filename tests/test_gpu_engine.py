@@ -27,10 +27,22 @@ def torch():
     return torch
 
 
-def _engine(shape, B, max_seq=96, page_size=16, verify_chunk=0, slots=None):
+def _engine(shape, B, max_seq=96, page_size=16, verify_chunk=0, slots=None, chain="0"):
+    """chain="1": the persistent layer-chain kernel (chain.cu) instead of the
+    separate GEMM / epilogue kernels (the choice is read at mg_init)."""
+    import os
+
     from paper_2605_30218_b200.engine import Engine
-    return Engine(shape, max_batch=B, max_slots=slots or B, max_seq=max_seq, page_size=page_size,
-                  verify_chunk=verify_chunk)
+    old = os.environ.get("MG_CHAIN")
+    os.environ["MG_CHAIN"] = chain
+    try:
+        return Engine(shape, max_batch=B, max_slots=slots or B, max_seq=max_seq, page_size=page_size,
+                      verify_chunk=verify_chunk)
+    finally:
+        if old is None:
+            del os.environ["MG_CHAIN"]
+        else:
+            os.environ["MG_CHAIN"] = old
 
 
 def _decode(torch, eng, prompts, steps, tau, prot=None, record=False):
@@ -110,8 +122,8 @@ def test_weights_bit_exact(orc, torch, tiny, tiny_gqa, which):
     eng.close()
 
 
-@pytest.mark.parametrize("which", ["tiny", "tiny_gqa"])
-def test_tau_inf_reference_and_batch_invariance(orc, torch, tiny, tiny_gqa, which):
+@pytest.mark.parametrize("which,chain", [("tiny", "0"), ("tiny_gqa", "0"), ("tiny", "1"), ("tiny_gqa", "1")])
+def test_tau_inf_reference_and_batch_invariance(orc, torch, tiny, tiny_gqa, which, chain):
     """tau=+inf (always-on verification) on the GPU: every row's sequence is
     bit-identical at batch 1, 3 and 8 (whatever shares the batch), and equals
     the oracle's deterministic reference outside the argmax-ambiguity band."""
@@ -123,7 +135,7 @@ def test_tau_inf_reference_and_batch_invariance(orc, torch, tiny, tiny_gqa, whic
         got = []
         for i0 in range(0, 8, B):
             group = prompts[i0:i0 + B]
-            eng = _engine(shp, len(group))
+            eng = _engine(shp, len(group), chain=chain)
             s, _ = _decode(torch, eng, group, steps, INF)
             st = eng.stats()
             assert st["triggers"] == st["protected_rows"] == len(group) * (steps - 1)   # r_verify = 1
@@ -138,14 +150,15 @@ def test_tau_inf_reference_and_batch_invariance(orc, torch, tiny, tiny_gqa, whic
     assert compared >= 0.6 * 8 * steps   # most tokens are outside the band on random-init logits
 
 
-def test_fast_logits_teacher_forced(orc, torch, tiny):
+@pytest.mark.parametrize("chain", ["0", "1"])
+def test_fast_logits_teacher_forced(orc, torch, tiny, chain):
     """tau=0 (pure BF16 batched, r_verify=0): the fast logits the GPU
     captures stay within 2e-2 of the oracle's, teacher-forced on the GPU's
     tokens; the fast argmax agrees outside the band."""
     shp, m = tiny
     B, steps = 6, 12
     prompts = inputs.prompts(B, inputs.ragged_lengths(B, 8, 20, seed=5), shp["vocab"], seed=40)
-    eng = _engine(shp, B)
+    eng = _engine(shp, B, chain=chain)
     cap = torch.empty((B, shp["vocab"]), dtype=torch.float32, device="cuda")
     eng.capture_logits(cap)
     st = orc.State(m, B, 64)
