@@ -60,8 +60,22 @@ class Clocks:
         self.index = index
         self.rows = []
         self.proc = None
+        self.nv = None
+        self.stop_ev = threading.Event()
 
     def start(self):
+        """Sample the SM clock and the throttle reasons every 5 ms through NVML
+        (nvidia-smi's 200 ms floor would give one sample of a short region)."""
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.t = threading.Thread(target=self._nvml, args=(h,), daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
@@ -71,11 +85,32 @@ class Clocks:
         except Exception:
             self.proc = None
 
+    def _nvml(self, h):
+        nv = self.nv
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = reasons(h)
+                self.rows.append(["", str(sm), str(mx), "", "", *["Active" if r & bits[k] else "Not Active"
+                                                                  for k in ("hw_slowdown", "hw_thermal_slowdown",
+                                                                            "sw_thermal_slowdown", "sw_power_cap")]])
+            except Exception:
+                pass
+            time.sleep(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def stop(self):
+        self.stop_ev.set()
+        if self.nv is not None:
+            self.t.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -92,7 +127,7 @@ class Clocks:
                     if v.strip().lower() == "active":
                         reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvml 5 ms" if self.nv else "nvidia-smi"}
 
 
 def _dist():
