@@ -131,12 +131,17 @@ static Sched sched_fast(const mg_ctx* c, int T, int max_ctx) {
   s.down = op_fast(c->d, c->F, T);
   s.lm = op_lm(c->V, c->d, T, false);
   // attention: one split per (token, kv head) once that fills ~2 CTAs per SM;
-  // smaller batches split the keys (>= 128 per split) to reach that
+  // smaller batches split the keys (>= 128 per split) to reach that.  Sized
+  // from the context CAPACITY (max_seq), not the current context, so the
+  // fast step's CUDA graph is the same for the whole decode (splits past a
+  // token's last key exit at once).
+  (void)max_ctx;
+  const int cap = c->cfg.max_seq;
   const int ctas = T * c->KV, target = 2 * kSMs;
   int ns = 1;
-  if (ctas < target) ns = clampi(cdiv(target, ctas), 1, cdiv(max_ctx, 128) > 1 ? cdiv(max_ctx, 128) : 1);
-  s.attn_sk = cdiv(cdiv(max_ctx, ns), 64) * 64;
-  s.attn_ns = cdiv(max_ctx, s.attn_sk);
+  if (ctas < target) ns = clampi(cdiv(target, ctas), 1, cdiv(cap, 128) > 1 ? cdiv(cap, 128) : 1);
+  s.attn_sk = cdiv(cdiv(cap, ns), 64) * 64;
+  s.attn_ns = cdiv(cap, s.attn_sk);
   return s;
 }
 
