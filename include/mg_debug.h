@@ -85,6 +85,12 @@ mg_status mgd_last_step(mg_ctx* ctx, int32_t* f_tok, float* g, float* v1, float*
                         int32_t* v_tok, float* v_g, uint8_t* kind, int32_t* out);
 /* Capture the fp32 fast logits [B][V] of subsequent steps into dev_buf (NULL: off). */
 mg_status mgd_capture_logits(mg_ctx* ctx, float* dev_buf);
+
+/* From the next step on, after each verifier LM head copy the fp32 logits of
+ * the gated rows into dev_buf[k][vocab], k = the row's rank among the step's
+ * gated rows (ascending batch index); nullptr stops.  Disables CUDA graphs
+ * while set.  For the tau calibration (eps_pert). */
+mg_status mgd_capture_verifier_logits(mg_ctx* ctx, float* dev_buf);
 /* Copy the weight tensor (layer, which) as the ORACLE's logical layout
  * (DESIGN.md 3.1 ids) to out_dev. */
 mg_status mgd_weight(mg_ctx* ctx, int32_t layer, int32_t which, uint16_t* out_dev, int64_t* n_host);

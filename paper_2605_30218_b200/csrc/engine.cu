@@ -551,7 +551,7 @@ static mg_status apply_pt(mg_ctx* c, const std::vector<std::pair<int, int>>& upd
 // the second, replayed afterwards (PDL edges are kept as programmatic edges).
 template <class F>
 static mg_status graphed(mg_ctx* c, const std::tuple<int, int, int, int, int, int>& key, F&& body) {
-  if (!c->use_graphs || c->timing.on || c->capture) return body();
+  if (!c->use_graphs || c->timing.on || c->capture || c->capture_v) return body();
   auto& g = c->graphs[key];
   if (g.exec) {
     CK(cudaGraphLaunch(g.exec, c->st));
@@ -597,8 +597,12 @@ static mg_status run_det(mg_ctx* c, int M, const std::vector<int>& last_host, in
       if (r1 > r0) {
         CK(launch_gather_rows_sub(c->xn, c->last_d + r0, c0, r1 - r0, c->d, c->xgn, c->st));
         c->launches++;
-        return lm_head(c, c->xgn, c->cfg.max_batch, r1 - r0, sc.lm, c->v_v1 + r0, c->v_tok + r0, c->v_v2 + r0,
-                       c->v_i2 + r0, c->v_g + r0);
+        mg_status rl = lm_head(c, c->xgn, c->cfg.max_batch, r1 - r0, sc.lm, c->v_v1 + r0, c->v_tok + r0,
+                               c->v_v2 + r0, c->v_i2 + r0, c->v_g + r0);
+        if (rl == MG_OK && c->capture_v)  // verifier logits of gated rows r0..r1 (rank order)
+          CK(cudaMemcpyAsync(c->capture_v + (size_t)r0 * c->V, c->logits, (size_t)(r1 - r0) * c->V * 4,
+                             cudaMemcpyDeviceToDevice, c->st));
+        return rl;
       }
       return MG_OK;
     });
@@ -1018,6 +1022,12 @@ mg_status mgd_last_step(mg_ctx* c, int32_t* f_tok, float* g, float* v1, float* v
 mg_status mgd_capture_logits(mg_ctx* c, float* dev_buf) {
   if (!c) return MG_ERR_INVALID;
   c->capture = dev_buf;
+  return MG_OK;
+}
+
+mg_status mgd_capture_verifier_logits(mg_ctx* c, float* dev_buf) {
+  if (!c) return MG_ERR_INVALID;
+  c->capture_v = dev_buf;
   return MG_OK;
 }
 

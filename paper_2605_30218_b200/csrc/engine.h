@@ -102,7 +102,8 @@ struct mg_ctx {
   int32_t *dbg_vtok, *dbg_out;
   float* dbg_vg;
   uint8_t *dbg_kind, *dbg_trig;
-  float* capture = nullptr;
+  float* capture = nullptr;    // fast logits [B][V] of the next steps (mgd_capture_logits)
+  float* capture_v = nullptr;  // verifier logits [gated rank][V] (mgd_capture_verifier_logits)
   int last_B = 0;
 
   // host mirrors

@@ -120,6 +120,12 @@ class Engine:
         check(lib().mgd_capture_logits(self.ctx, C.c_void_p(buf.data_ptr()) if buf is not None else None),
               self.ctx, "capture")
 
+    def capture_verifier_logits(self, buf):
+        """Debug: verifier fp32 logits of the gated rows of the next steps into
+        buf [max_batch, vocab] (rank order, include/mg_debug.h); None stops."""
+        check(lib().mgd_capture_verifier_logits(self.ctx, C.c_void_p(buf.data_ptr()) if buf is not None else None),
+              self.ctx, "capture_verifier_logits")
+
     def weight(self, layer: int, which: int):
         n = C.c_int64(0)
         check(lib().mgd_weight(self.ctx, layer, which, None, C.byref(n)), self.ctx, "mgd_weight")
