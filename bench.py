@@ -61,6 +61,7 @@ class Clocks:
         self.rows = []
         self.proc = None
         self.nv = None
+        self.err = None
         self.stop_ev = threading.Event()
 
     def start(self):
@@ -95,12 +96,18 @@ class Clocks:
         while not self.stop_ev.is_set():
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            except Exception as e:  # noqa: BLE001
+                self.err = repr(e)
+                sm = None
+            try:
                 r = reasons(h)
+            except Exception as e:  # noqa: BLE001
+                self.err = repr(e)
+                r = 0
+            if sm is not None:
                 self.rows.append(["", str(sm), str(mx), "", "", *["Active" if r & bits[k] else "Not Active"
                                                                   for k in ("hw_slowdown", "hw_thermal_slowdown",
                                                                             "sw_thermal_slowdown", "sw_power_cap")]])
-            except Exception:
-                pass
             time.sleep(0.005)
 
     def _read(self):
@@ -126,8 +133,11 @@ class Clocks:
                 for n, v in zip(names, r[5:9]):
                     if v.strip().lower() == "active":
                         reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm), "source": "nvml 5 ms" if self.nv else "nvidia-smi"}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": sorted(reasons), "samples": len(sm), "source": "nvml 5 ms" if self.nv else "nvidia-smi"}
+        if getattr(self, "err", None):
+            out["error"] = self.err
+        return out
 
 
 def _dist():
@@ -186,10 +196,16 @@ def run_gpu(args):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         outs = torch.empty((K, B), dtype=torch.int32, device="cuda")
+        prof = clocks is not None and os.environ.get("MG_PROFILE_TIMED") == "1"  # ncu --profile-from-start off
+        if prof:
+            torch.cuda.profiler.start()
         e0.record(stream)
         for k in range(K):
             eng.step(list(range(B)), prot, tau, outs[k], kind)
         e1.record(stream)
+        if prof:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.stop()
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
@@ -303,7 +319,8 @@ def run_gpu(args):
                 "margingate_tok_s": round(tok / (T[mg] * 1e-3), 2),
                 "always_on_tok_s": round(tok / (T[ao] * 1e-3), 2),
                 "inc_margingate": round(inc_mg, 4), "inc_always_on": round(inc_ao, 4),
-                "increment_ratio": round(metrics.increment_ratio(inc_ao, inc_mg), 3) if inc_mg > 0.01 else None,
+                "increment_ratio": (round(metrics.increment_ratio(inc_ao, inc_mg), 3)
+                                    if stats[mg]["triggers"] > 0 and inc_mg > 0 else None),
                 "trigger_pct": round(100 * rt["r_verify"], 3), "repair_pct": round(100 * rt["r_repair"], 4),
                 "determinism_pct": round(100 * detv[0] / detv[1], 2) if detv[1] else None,
                 "verifier_launches": stats[mg]["verifier_launches"], "catchup_tokens": stats[mg]["catchup_tokens"]}

@@ -92,11 +92,24 @@ int streamk_G(int N, int K) {
   return clampi(W / 4, 1, kSMs);
 }
 
+// fast path: CUDA-core GEMV for T <= this many tokens.  Default 0: the
+// tcgen05 kernel with a 16-token tile is faster at every batch size measured
+// (llama8b step, B=2: 3.29 vs 5.15 ms; B=4: 3.37 vs 8.11 ms).
+// MG_FAST_GEMV_MAX re-enables the GEMV (measurement knob).
+int gemv_max_tokens() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MG_FAST_GEMV_MAX");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 OpSched op_fast(int N, int K, int T) {
   OpSched o;
   o.N = N;
   o.K = K;
-  o.impl = T <= 4 ? 1 : 0;
+  o.impl = T <= gemv_max_tokens() ? 1 : 0;
   o.tile_n = gemm_tile_n(T);
   o.mma_n = o.tile_n;
   o.splits = o.impl == 1 ? splits_for(N, K, T, o.tile_n, o.impl) : 1;
@@ -141,6 +154,7 @@ static Sched sched_fast(const mg_ctx* c, int T, int max_ctx) {
   int ns = 1;
   if (ctas < target) ns = clampi(cdiv(target, ctas), 1, cdiv(cap, 128) > 1 ? cdiv(cap, 128) : 1);
   s.attn_sk = cdiv(cdiv(cap, ns), 64) * 64;
+  if (c->fast_sk_override > 0) s.attn_sk = c->fast_sk_override;  // measurement knob (MG_FAST_SK)
   s.attn_ns = cdiv(cap, s.attn_sk);
   return s;
 }
@@ -152,8 +166,8 @@ static Sched sched_det(const mg_ctx* c, int T, int max_ctx) {
   s.gu = op_det(2 * c->F, c->d, T);
   s.down = op_det(c->d, c->F, T);
   s.lm = op_lm(c->V, c->d, T, true);
-  s.attn_sk = kDetSplitKeys;  // pinned verifier attention split (A14)
-  s.attn_ns = cdiv(max_ctx, kDetSplitKeys);
+  s.attn_sk = c->det_sk;  // pinned verifier attention split (A14)
+  s.attn_ns = cdiv(max_ctx, s.attn_sk);
   return s;
 }
 
@@ -176,6 +190,10 @@ struct Layout {
 
 static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout* lay) {
   const mg_config& g = c->cfg;
+  {
+    const char* ds = getenv("MG_DET_SK");  // measurement knob; sizes the split partials below
+    c->det_sk = ds && atoi(ds) >= 64 ? atoi(ds) / 64 * 64 : kDetSplitKeys;
+  }
   c->L = g.n_layers; c->d = g.d_model; c->H = g.n_heads; c->KV = g.n_kv_heads; c->hd = g.head_dim;
   c->F = g.d_ff; c->V = g.vocab;
   c->NQ = c->H * c->hd; c->NK = c->KV * c->hd; c->NQKV = c->NQ + 2 * c->NK;
@@ -220,7 +238,7 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   upd(sched_det(c, c->Tv, g.max_seq), c->Tv);
   c->part_elems = pe;
   size_t attn_rows_fast = (size_t)g.max_batch * c->H * cdiv(g.max_seq, 64);
-  size_t attn_rows_det = (size_t)c->Tv * c->H * cdiv(g.max_seq, kDetSplitKeys);
+  size_t attn_rows_det = (size_t)c->Tv * c->H * cdiv(g.max_seq, c->det_sk);
   size_t attn_rows = attn_rows_fast > attn_rows_det ? attn_rows_fast : attn_rows_det;
 
   Carver s(ws);
@@ -748,6 +766,8 @@ mg_status mg_init(const mg_config* cfg, const mg_buffers* bufs, void* stream, mg
     // (DESIGN.md section 7.4); MG_CHAIN=1 selects it for A/B measurements
     const char* e = getenv("MG_CHAIN");
     c->use_chain = e && e[0] == '1';
+    const char* fs = getenv("MG_FAST_SK");  // measurement knobs: attention split sizes
+    c->fast_sk_override = fs ? atoi(fs) : 0;
     const char* f = getenv("MG_CHAIN_PF");  // A/B knob: L2 run-ahead in 16 KB k-blocks
     c->chain_pf = f ? atoi(f) : 0;
   }

@@ -80,7 +80,9 @@ struct mg_ctx {
   bool use_chain = false;                // MG_CHAIN=1: persistent layer chain (A/B only; slower today)
   unsigned long long* chain_trace = nullptr;  // diagnostics (mgd_chain_trace)
   int chain_trace_layer = -2;
-  int chain_pf = 0;  // chain L2 run-ahead (k-blocks per CTA; measured harmful, off)
+  int chain_pf = 0;
+  int fast_sk_override = 0;  // MG_FAST_SK (measurement)
+  int det_sk = 512;          // verifier attention keys per split (A14; MG_DET_SK for measurement)  // chain L2 run-ahead (k-blocks per CTA; measured harmful, off)
   CUtensorMap attn_qmap, kv_map[2];      // TMA maps: q [Tmax][H][hd]; pools (fast, shadow)
   float *rope_cos, *rope_sin;
   size_t part_elems;
