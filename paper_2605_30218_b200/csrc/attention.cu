@@ -32,6 +32,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "epilogue.cuh"
 #include "kernels.h"
 
 namespace mg {
@@ -49,7 +50,8 @@ struct AtCfg {
   static constexpr int Q_OFF = 0;
   static constexpr int RING_OFF = BLK;
   static constexpr int ML_OFF = RING_OFF + (RING > XG ? RING : XG);  // m, l: [warp][16] each
-  static constexpr int BAR_OFF = ML_OFF + 2 * 64 * 4;                 // Q, then [warp][R]
+  static constexpr int KVN_OFF = ML_OFF + 2 * 64 * 4;                // fused QKV: new K and V rows [2][HD] bf16
+  static constexpr int BAR_OFF = KVN_OFF + 2 * HD * 2;                // Q, then [warp][R]
   static constexpr int SMEM = BAR_OFF + (1 + 4 * R) * 8 + 8 + 1024;   // + flag + alignment slack
 };
 
@@ -152,19 +154,67 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
     }
     griddep();
   }
-  if (warp == 0 && lane == 0) {
-    mbar_expect_tx(&bars[0], C::BLK);
+  for (int i = issued; i < R && i < nbw; ++i) issue(i);  // the remaining first blocks (after the wait)
+  uint16_t* kvn = reinterpret_cast<uint16_t*>(sm + C::KVN_OFF);
+  const bool has_new = a.fuse_qkv && sp == n_sp - 1;  // this CTA holds key n - 1
+  if (!a.fuse_qkv) {
+    if (warp == 0 && lane == 0) {
+      mbar_expect_tx(&bars[0], C::BLK);
 #pragma unroll
-    for (int h = 0; h < C::HALVES; ++h) tma_load_3d(sm + C::Q_OFF + h * 2048, &a.qmap, &bars[0], 64 * h, kvh * G, t);
+      for (int h = 0; h < C::HALVES; ++h)
+        tma_load_3d(sm + C::Q_OFF + h * 2048, &a.qmap, &bars[0], 64 * h, kvh * G, t);
+    }
+  } else {
+    // QKV epilogue (the same arithmetic as k_epi_qkv): q rows of
+    // the G heads into the swizzled Q tile; the new K/V column (RoPE on K) into
+    // kvn and appended to the cache at position p = n - 1
+    constexpr int h2 = HD / 2;
+    const int NQKV = (H + 2 * a.KV) * HD;
+    const size_t stride = (size_t)a.T * NQKV, row = (size_t)t * NQKV;
+    const int p = a.pos[t];
+    const int nq = G * h2, nitems = nq + (has_new ? 2 * h2 : 0);
+    for (int w = threadIdx.x; w < nitems; w += kAtThreads) {
+      const bool isq = w < nq;
+      const int g = isq ? w / h2 : (w - nq) / h2;  // q: head in group; k/v: 0 = K, 1 = V
+      const int i = (isq ? w : w - nq) % h2;
+      const int h = isq ? kvh * G + g : H + g * a.KV + kvh;
+      const int f1 = h * HD + i, f2 = f1 + h2;
+      float x = sum_splits(a.qkv_part, part_count(a.qkv_ps, f1), stride, row + f1);
+      float y = sum_splits(a.qkv_part, part_count(a.qkv_ps, f2), stride, row + f2);
+      if (a.bias) {
+        x = __fadd_rn(x, bf2f(a.bias[f1]));
+        y = __fadd_rn(y, bf2f(a.bias[f2]));
+      }
+      uint16_t oa, ob;
+      if (isq || g == 0) {  // RoPE on q and k
+        const float c = a.rcos[(size_t)p * h2 + i], sn = a.rsin[(size_t)p * h2 + i];
+        oa = f2bf(__fsub_rn(__fmul_rn(x, c), __fmul_rn(y, sn)));
+        ob = f2bf(__fadd_rn(__fmul_rn(y, c), __fmul_rn(x, sn)));
+      } else {
+        oa = f2bf(x);
+        ob = f2bf(y);
+      }
+      if (isq) {
+        uint8_t* qt = sm + C::Q_OFF;
+        *reinterpret_cast<uint16_t*>(qt + swz(g, i) + (i & 7) * 2) = oa;
+        *reinterpret_cast<uint16_t*>(qt + swz(g, i + h2) + ((i + h2) & 7) * 2) = ob;
+      } else {
+        kvn[g * HD + i] = oa;
+        kvn[g * HD + i + h2] = ob;
+        uint16_t* dst = cache_ptr(a.cache, a.slot[t], p, g, kvh);
+        dst[i] = oa;
+        dst[i + h2] = ob;
+      }
+    }
+    __syncthreads();
   }
-  for (int i = issued; i < R && i < nbw; ++i) issue(i);
 
   const int rr = lane & 7, mi = lane >> 3;
   const int r0 = lane >> 2, r1 = r0 + 8, cc = 2 * (lane & 3);
   // ---- Q tile (A operand; rows >= G are other heads / zero fill, ignored).
   // Its fragments are re-read from shared memory per block (ldmatrix) rather
   // than held in registers, which keeps the kernel at 4 CTAs per SM.
-  mbar_wait(&bars[0], 0);
+  if (!a.fuse_qkv) mbar_wait(&bars[0], 0);
   const uint32_t qa = smem_u32(sm + C::Q_OFF);
   const float scale = (float)(1.0 / sqrt((double)HD));
 
@@ -184,6 +234,15 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
       for (int e = lane; e < (16 - valid) * C::HALVES * 8; e += 32) {
         const int row = valid + e / (C::HALVES * 8), rem = e % (C::HALVES * 8);
         reinterpret_cast<uint4*>(st + C::BLK + (rem >> 3) * 2048 + row * 128)[rem & 7] = make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+    }
+    if (has_new && lo + 16 * (warp + 4 * i) + 16 >= n) {  // the block holding key n - 1: patch its K/V row
+      const int rr = n - 1 - (lo + 16 * (warp + 4 * i));
+      for (int e = lane; e < 2 * (HD / 8); e += 32) {
+        const int sel = e / (HD / 8), col = (e % (HD / 8)) * 8;
+        *reinterpret_cast<uint4*>(st + sel * C::BLK + swz(rr, col)) =
+            *reinterpret_cast<const uint4*>(kvn + sel * HD + col);
       }
       __syncwarp();
     }

@@ -378,14 +378,22 @@ static mg_status forward(mg_ctx* c, int T, const int32_t* slot, const int32_t* p
     mg_status r = gemm(c, c->xn, Tm, T, w.qkv, sc.qkv, c->part);
     if (r) return r;
     CacheView cv = cache_view(c, which, l);
-    CK(launch_epi_qkv(c->part, sc.qkv.ps(), w.bqkv, pos, T, c->H, c->KV, c->hd, c->rope_cos, c->rope_sin, c->q,
-                      &cv, slot, nullptr, nullptr, c->st));
+    // fast path: the QKV epilogue runs inside the attention kernel (one new
+    // column per token); the verifier's catch-up chunks append several columns
+    // of one sequence per launch, so they keep the separate epilogue kernel
+    const bool fuse = which == 0;
+    if (!fuse)
+      CK(launch_epi_qkv(c->part, sc.qkv.ps(), w.bqkv, pos, T, c->H, c->KV, c->hd, c->rope_cos, c->rope_sin, c->q,
+                        &cv, slot, nullptr, nullptr, c->st));
     AttnArgs aa{};
     aa.q = c->q; aa.cache = cv; aa.paged = 1; aa.slot = slot; aa.n_keys = nk;
     aa.T = T; aa.H = c->H; aa.KV = c->KV; aa.hd = c->hd; aa.split_keys = sc.attn_sk; aa.n_splits = sc.attn_ns;
     aa.part_acc = c->attn_acc; aa.part_ml = c->attn_ml; aa.out = c->att;
     aa.qmap = c->attn_qmap; aa.kmap = aa.vmap = c->kv_map[which]; aa.counter = c->attn_cnt;
     aa.prewait = which == 0;  // fast path: each token appended only its own column
+    aa.fuse_qkv = fuse;
+    aa.qkv_part = c->part; aa.qkv_ps = sc.qkv.ps(); aa.bias = w.bqkv; aa.pos = pos;
+    aa.rcos = c->rope_cos; aa.rsin = c->rope_sin;
     size_t i0 = 0;
     if (c->timing.on) { i0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
     CK(launch_attention(aa, c->st));
@@ -401,7 +409,7 @@ static mg_status forward(mg_ctx* c, int T, const int32_t* slot, const int32_t* p
     // residual + the NEXT norm (next layer's attn_norm, or the final norm)
     const uint16_t* wn = l + 1 < c->L ? c->layers[l + 1].attn_norm : c->final_norm;
     CK(launch_residual_norm(c->x, c->part, sc.down.ps(), T, c->d, wn, eps, c->xn, c->st));
-    c->launches += 5;
+    c->launches += fuse ? 4 : 5;
   }
   return MG_OK;
 }

@@ -126,6 +126,17 @@ struct AttnArgs {
   uint16_t* out;          // [T][H*hd]
   int32_t prewait;        // 1: keys < n_keys-1 predate the previous kernel (fast path: one new column
                           //    per token) and may be read before griddepcontrol.wait
+  // fused QKV epilogue (fast path, one new column per token): the CTA builds
+  // the q rows of its G query heads from the QKV GEMM partials (bias, RoPE,
+  // bf16) in shared memory, and the CTA holding key n-1 builds the new K/V
+  // column, appends it to the cache at pos[t] and patches it into its tile
+  int32_t fuse_qkv;
+  const float* qkv_part;  // [slots][T][(H+2KV)*hd]
+  PartSpec qkv_ps;
+  const uint16_t* bias;   // nullable
+  const int32_t* pos;     // [T] (= n_keys - 1)
+  const float* rcos;      // RoPE tables [max_pos][hd/2]
+  const float* rsin;
 };
 bool make_tmap_3d(CUtensorMap* m, const void* base, int d0, int64_t d1, int64_t d2, int box1);
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st);
