@@ -324,7 +324,7 @@ def test_api_errors(torch, tiny):
 def test_wide_shallow_parity(orc, torch):
     """8B widths (d 4096, d_ff 14336, GQA 32/8, hd 128), 2 layers, full
     128256 vocabulary: tau=0 fast logits within 2e-2 teacher-forced at batch
-    4 (CUDA-core GEMMs) and 24 (tcgen05), and the tau=inf sequence equals
+    4 and 24 (tcgen05 token tiles 16 and 32), and the tau=inf sequence equals
     the oracle reference outside the band."""
     shp = inputs.shape("wide")
     m = orc.Model(shp)
@@ -357,4 +357,30 @@ def test_wide_shallow_parity(orc, torch):
     seqs, _ = _decode(torch, eng, [p], 6, INF)
     toks, gs = _oracle_reference(orc, m, p, 6)
     assert _agree_until_band(seqs[0], toks, gs) >= 1
+    eng.close()
+
+
+@pytest.mark.parametrize("which,B", [("tiny", 6), ("wide", 4)])
+def test_fast_path_equals_verifier_when_splits_agree(torch, which, B):
+    """the fast GEMMs use the verifier's weight-shape-fixed
+    stream-K partition and a token column's tcgen05 result does not depend on
+    the MMA width, so whenever the attention splits also agree (here: short
+    contexts, one split per token on both paths) the fast logits equal the
+    verifier's logits bit for bit (tau=inf, all rows protected: verifier rank
+    k = row k)."""
+    shp = inputs.shape(which)
+    prompts = inputs.prompts(B, inputs.ragged_lengths(B, 5, 12, seed=3), shp["vocab"], seed=900)
+    eng = _engine(shp, B, max_seq=32)
+    capf = torch.empty((B, shp["vocab"]), dtype=torch.float32, device="cuda")
+    capv = torch.empty((B, shp["vocab"]), dtype=torch.float32, device="cuda")
+    for i, p in enumerate(prompts):
+        eng.prefill(i, p)
+    eng.capture_logits(capf)
+    eng.capture_verifier_logits(capv)
+    out = torch.empty(B, dtype=torch.int32, device="cuda")
+    for _ in range(4):
+        eng.step(list(range(B)), None, INF, out)
+        assert torch.equal(capf, capv)
+    st = eng.stats()
+    assert st["repairs"] == 0 and st["triggers"] == st["protected_rows"] == 4 * B
     eng.close()
