@@ -365,7 +365,7 @@ def run_gpu(args):
         "arms": arms_out,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": hbm,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4) if achieved else None,
-                     "traffic": traffic, "kernel": "k_gemm_tc/k_gemm_cc (weight-streaming GEMM class, fast path)",
+                     "traffic": traffic, "kernel": "k_gemm_tc (weight-streaming GEMM class, fast path)",
                      "peak_source": peak_src, "gemm_launches": tim["gemm_launches"],
                      "gemm_us_per_launch": round(1e3 * tim["gemm_ms"] / max(tim["gemm_launches"], 1), 2),
                      "gemm_ms_per_step": round(tim["gemm_ms"] / K, 4),
