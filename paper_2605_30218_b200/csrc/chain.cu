@@ -40,8 +40,11 @@
 
 namespace mg {
 
-constexpr int kChainThreads = 384;
-constexpr int kOpThreads = 288;  // warps 2-5 and 7-11
+#ifndef MG_CHAIN_WARPS
+#define MG_CHAIN_WARPS 12
+#endif
+constexpr int kChainThreads = 32 * MG_CHAIN_WARPS;
+constexpr int kOpThreads = kChainThreads - 96;  // warps 2-5 and 7.. (the epilogue warps + the op helpers)
 
 MG_DEV uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
@@ -62,14 +65,14 @@ MG_DEV bool wait_count(const uint32_t* p, uint32_t target, int32_t* err) {
   return true;
 }
 MG_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-MG_DEV void op_bar() { asm volatile("bar.sync 2, 288;" ::: "memory"); }
+MG_DEV void op_bar() { asm volatile("bar.sync 2, %0;" ::"n"(kOpThreads) : "memory"); }
 
 template <int TN>
 struct ChainCfg {
   using G = GemmTcCfg<TN>;
   static constexpr int NS = G::NS;
   // 1 KB alignment slack, the ring, then fullA/fullB/empty[NS], tfull/tempty[2], tmem slot, norm scratch
-  static constexpr int SMEM_FIXED = 1024 + NS * G::STAGE + (3 * NS + 4) * 8 + 128;  // + 8 B per token
+  static constexpr int SMEM_FIXED = 1024 + NS * G::STAGE + (3 * NS + 4) * 8 + 192;  // + 8 B per token
 };
 
 // ---- phase ops, run by the 288 op threads of every CTA (otid 0..287).  They
@@ -95,6 +98,26 @@ MG_DEV OpDesc op_desc(const ChainPhase& ph) {
   return d;
 }
 
+// 8 consecutive partial sums, slots added in k order, 4 slots' loads in flight
+MG_DEV void sum8_slots4(const float* __restrict__ part, int S, size_t stride, size_t idx, float* a) {
+  for (int s0 = 0; s0 < S; s0 += 4) {
+    float4 lo[4], hi[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (s0 + u < S) {
+        lo[u] = __ldcg(reinterpret_cast<const float4*>(part + (size_t)(s0 + u) * stride + idx));
+        hi[u] = __ldcg(reinterpret_cast<const float4*>(part + (size_t)(s0 + u) * stride + idx + 4));
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (s0 + u < S) {
+        const float v[8] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w, hi[u].x, hi[u].y, hi[u].z, hi[u].w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = (s0 + u == 0) ? v[k] : __fadd_rn(a[k], v[k]);
+      }
+  }
+}
+
 MG_DEV void op_resnorm(const OpDesc& ph, int T, const PartSpec& ps, int otid, float* red, float* s_inv) {
   const int d = ph.N, nv = d / 8;
   const size_t stride = (size_t)T * d;
@@ -105,7 +128,7 @@ MG_DEV void op_resnorm(const OpDesc& ph, int T, const PartSpec& ps, int otid, fl
     for (int i = otid; i < nv; i += kOpThreads) {
       float acc[8];
       const uint4 x0 = __ldcg(xv + i);
-      sum8_pieces(ph.part, part_count(ps, i * 8), stride, (size_t)r * d + (size_t)i * 8, acc);
+      sum8_slots4(ph.part, part_count(ps, i * 8), stride, (size_t)r * d + (size_t)i * 8, acc);
       const uint4 h = residual8(x0, acc);
       xv[i] = h;
       ss = ss8(h, ss);
@@ -173,8 +196,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   uint64_t* tfull = empty + NS;   // [2]
   uint64_t* tempty = tfull + 2;   // [2]
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  float* red = (float*)(tmem_slot + 2);  // [13] op-warp partials
-  float* s_inv = red + 16;
+  float* red = (float*)(tmem_slot + 2);  // [kOpThreads / 32] op-warp partials
+  float* s_inv = red + 32;
   uint32_t* s_epoch = (uint32_t*)(s_inv + 1);
   int* tok_pos = (int*)(s_epoch + 4);  // [T] staged token positions (QKV ops), then [T] their KV pages
   int* tok_page = tok_pos + a.T;
@@ -206,7 +229,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
   int qkv_ph = -1;
   for (int p = 0; p < a.n_ph; ++p)
     if (a.ph[p].op == CH_QKV) qkv_ph = p;
-  if (qkv_ph >= 0 && threadIdx.x >= 224) {
+  if (qkv_ph >= 0 && threadIdx.x >= 224) {  // the op-helper warps
     const QkvArgs& q = a.ph[qkv_ph].qkv;
     for (int t = threadIdx.x - 224; t < a.T; t += kChainThreads - 224) {
       const int p = q.pos[t];
@@ -367,7 +390,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
     // keep every counter of this epoch in step: arrive on the unused ones
     if (ltid == 0)
       for (int k = 2 * a.n_ph; k < 2 * kChainMax; ++k) atomicAdd(&a.sync[k], 1u);
-  } else if (warp >= 7) {
+  } else if (warp >= 7) {  // warps 7 .. MG_CHAIN_WARPS-1
     // ---- op helpers: one op per phase, between the epilogue's two op_bar()s
     const int otid = 128 + threadIdx.x - 224;
     for (int p = 0; p < a.n_ph; ++p) {
