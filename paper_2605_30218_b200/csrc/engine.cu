@@ -116,13 +116,27 @@ OpSched op_fast(int N, int K, int T) {
   o.G = o.impl == 1 ? 0 : streamk_G(N, K);
   return o;
 }
+bool det_mma16() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MG_DET_MMA16");
+    v = e && e[0] == '1';
+  }
+  return v == 1;
+}
+
 OpSched op_det(int N, int K, int T) {
   OpSched o;
   o.N = N;
   o.K = K;
   o.impl = 0;
   o.tile_n = gemm_tile_n(T);
-  o.mma_n = 16;                 // pinned 16-column slot groups
+  // one MMA per k-step across the whole token tile: a token column's fp32
+  // result does not depend on the instruction width nor on its slot (tested
+  // for N = 16..256, tests/test_gpu_ops.py::test_gemm_column_invariance), so
+  // only the M128 x K16 shape and the partition below need pinning.
+  // MG_DET_MMA16=1 restores the 16-column slot groups (measurement knob).
+  o.mma_n = det_mma16() ? 16 : o.tile_n;
   o.splits = 1;
   o.G = streamk_G(N, K);        // partition depends on the weight shape only
   return o;

@@ -22,11 +22,12 @@
 // SwiGLU, top-2) run in the consumer kernels in k order, so results are
 // run-to-run deterministic (no float atomics).
 //
-// Batch invariance (BASELINE north_star, A14): the verifier uses a
-// partition fixed per weight shape and MMA16 (every token column produced by
-// M128 x N16 x K16 instructions over the same k-blocks in the same order,
-// whatever the batch); tested bit-exact in
-// tests/test_gpu_ops.py::test_gemm_column_invariance.
+// Batch invariance (BASELINE north_star, A14): the partition is a
+// function of the weight shape only, and a token column's fp32 result does
+// not depend on the instruction width N, its slot or the other columns
+// (tests/test_gpu_ops.py::test_gemm_column_invariance: N = 16..256), so the
+// verifier runs the same full-width MMAs as the fast path.  MMA16 (16-column
+// instructions per slot group) remains as an option.
 //
 // k_gemm_cc: CUDA-core kernel for T <= 8 tokens (the fast path's tiny-batch
 // choice): warp per output row, 128-bit weight loads, fp32 FMA, fixed

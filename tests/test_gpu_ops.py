@@ -139,9 +139,10 @@ def test_gemm_cuda_core(orc, K, T):
 
 
 def test_gemm_column_invariance(orc, K):
-    """Verifier GEMM (mma_n = 16, fixed split): a token's output is bit-identical
-    whatever other tokens share the launch, wherever its column sits, for any
-    T and tile width (BASELINE north_star: bit-identical at batch 1..B)."""
+    """Verifier GEMM (fixed split): a token's output is bit-identical whatever
+    other tokens share the launch, wherever its column sits, for any T, tile
+    width and MMA instruction width (16 columns or the whole tile) --
+    BASELINE north_star: bit-identical at batch 1..B."""
     rng = np.random.default_rng(77)
     N, K_ = 256, 2048
     W = _rand(orc, rng, (N, K_), 1 / np.sqrt(K_))
@@ -154,9 +155,11 @@ def test_gemm_column_invariance(orc, K):
                 x = others.copy()
                 x[col] = target[0]
                 for tile in (16, 32, 64, 128, 256):
-                    part = K.gemm(x, W, splits=splits, impl=0, mma_n=16, tile_n=tile)
-                    ok = np.isnan(ref) == np.isnan(part[:, col])
-                    assert ok.all() and np.array_equal(np.nan_to_num(part[:, col]), np.nan_to_num(ref)), (T, col, tile)
+                    for mma in sorted({16, tile}):
+                        part = K.gemm(x, W, splits=splits, impl=0, mma_n=mma, tile_n=tile)
+                        ok = np.isnan(ref) == np.isnan(part[:, col])
+                        assert ok.all() and np.array_equal(np.nan_to_num(part[:, col]), np.nan_to_num(ref)), \
+                            (T, col, tile, mma)
 
 
 # ------------------------------------------------------------------ a3 epilogue
