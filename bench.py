@@ -72,6 +72,8 @@ class Clocks:
             pynvml.nvmlInit()
             self.nv = pynvml
             h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.h = h
+            self._sample(h)  # one synchronous sample at the start of the region
             self.t = threading.Thread(target=self._nvml, args=(h,), daemon=True)
             self.t.start()
             return
@@ -86,28 +88,30 @@ class Clocks:
         except Exception:
             self.proc = None
 
-    def _nvml(self, h):
+    def _sample(self, h):
         nv = self.nv
         bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                 "sw_power_cap": 0x4}
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
         reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        try:
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+            return
+        try:
+            r = reasons(h)
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+            r = 0
+        self.rows.append(["", str(sm), str(mx), "", "", *["Active" if r & bits[k] else "Not Active"
+                                                          for k in ("hw_slowdown", "hw_thermal_slowdown",
+                                                                    "sw_thermal_slowdown", "sw_power_cap")]])
+
+    def _nvml(self, h):
         while not self.stop_ev.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-            except Exception as e:  # noqa: BLE001
-                self.err = repr(e)
-                sm = None
-            try:
-                r = reasons(h)
-            except Exception as e:  # noqa: BLE001
-                self.err = repr(e)
-                r = 0
-            if sm is not None:
-                self.rows.append(["", str(sm), str(mx), "", "", *["Active" if r & bits[k] else "Not Active"
-                                                                  for k in ("hw_slowdown", "hw_thermal_slowdown",
-                                                                            "sw_thermal_slowdown", "sw_power_cap")]])
+            self._sample(h)
             time.sleep(0.005)
 
     def _read(self):
@@ -115,6 +119,8 @@ class Clocks:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def stop(self):
+        if self.nv is not None:
+            self._sample(self.h)  # and one at its end (the sampler thread may not have run)
         self.stop_ev.set()
         if self.nv is not None:
             self.t.join(timeout=2)
