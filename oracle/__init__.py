@@ -96,6 +96,9 @@ def lib():
                 "or_state_column": (None, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, u16p]),
                 "or_state_digest": (C.c_uint64, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32]),
                 "or_state_stats": (None, [C.c_void_p, u64p]),
+                "or_state_set_repair_mode": (None, [C.c_void_p, C.c_int32]),
+                "or_verify_window": (C.c_int32, [C.c_void_p, i32p, C.c_int32, _P(Sched), i32p, i32p, i32p]),
+                "or_state_window_stats": (None, [C.c_void_p, u64p]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -342,6 +345,24 @@ class State:
         keys = ["steps", "rows", "protected_rows", "triggers", "verified", "repairs", "verifier_launches",
                 "catchup_tokens", "nan"]
         return {k: int(v) for k, v in zip(keys, out)}
+
+    def set_repair_mode(self, mode: int):
+        """0 column repair, 1 token-only ablation."""
+        lib().or_state_set_repair_mode(self._h, int(mode))
+
+    def verify_window(self, rows, det: Sched):
+        """LLM-42-style windowed verify + rollback.
+        Returns (new_pos, last_tok, rolled_back) per row."""
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        n = rows.size
+        npos, last, rb = np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n, np.int32)
+        lib().or_verify_window(self._h, i32(rows), n, C.byref(det), i32(npos), i32(last), i32(rb))
+        return npos, last, rb
+
+    def window_stats(self):
+        out = np.zeros(3, np.uint64)
+        lib().or_state_window_stats(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)))
+        return {k: int(v) for k, v in zip(["window_rows", "rollbacks", "rolled_back_tokens"], out)}
 
     def close(self):
         if self._h:

@@ -438,7 +438,9 @@ struct or_state {
   int32_t* hist;        /* [row][max_seq + 1]: committed token consumed at position q */
   int32_t* pos;         /* next decode position p (= columns in the fast cache) */
   int32_t* shadow_len;  /* columns of the shadow cache that are final */
+  int32_t repair_mode;  /* 0 column repair, 1 token-only ablation */
   uint64_t stats[9];
+  uint64_t wstats[3];   /* window verifies (rows), rollbacks, rolled-back tokens */
 };
 
 static inline int64_t kv_index(const or_state* s, int32_t row, int32_t l, int32_t kvsel, int32_t h, int32_t q) {
@@ -633,7 +635,7 @@ int32_t or_step(or_state* s, const int32_t* rows, int32_t B, const uint8_t* prot
     } else if (!tr[b]) { k = 0; out = ft[b]; }
     else if (vt[b] == ft[b]) { k = 1; out = ft[b]; }
     else { k = 2; out = vt[b]; }
-    if (k == 2) copy_column(s, 1, 0, r, p);
+    if (k == 2 && s->repair_mode == 0) copy_column(s, 1, 0, r, p);
     s->hist[(int64_t)r * (s->max_seq + 1) + p + 1] = out;
     s->pos[r] = p + 1;
     if (kind) kind[b] = k;
@@ -684,3 +686,59 @@ uint64_t or_state_digest(const or_state* s, int32_t which, int32_t skip_row, int
 }
 
 void or_state_stats(const or_state* s, uint64_t* out9) { memcpy(out9, s->stats, sizeof(s->stats)); }
+
+/* Repair-action ablation (S4.4 "Repair-action ablation"): mode 1
+ * emits the verifier token but leaves the tentative BF16 K/V column in place
+ * ("token-only"); mode 0 (default) copies the verifier-produced column. */
+void or_state_set_repair_mode(or_state* s, int32_t mode) { s->repair_mode = mode; }
+
+/* LLM-42-style windowed verification with rollback ("keeps the
+ * default path but verifies every token", "verifier setting
+ * K=64", "restart-from-rollback"), in the
+ * shadow-cache reading A1.  For each row r in rows[0..n):
+ *   the tokens committed since the last verification, hist[shadow_len+1..pos],
+ *   are checked in order: for q = shadow_len .. pos-1 the deterministic
+ *   forward consumes hist[q] at position q (shadow cache) and its argmax v
+ *   predicts position q+1.  At the first q with v != hist[q+1] the row rolls
+ *   back: hist[q+1] = v, pos = shadow_len = q+1 (the tokens after q+1 are
+ *   discarded; fast columns >= q+1 are rewritten by later steps).  Without a
+ *   mismatch shadow_len = pos.
+ * Outputs (nullable): new_pos[i] = pos after the call, last_tok[i] =
+ * hist[new_pos], rolled_back[i] = tokens discarded.  Returns the total number
+ * of discarded tokens. */
+int32_t or_verify_window(or_state* s, const int32_t* rows, int32_t n, const or_sched* det, int32_t* new_pos,
+                         int32_t* last_tok, int32_t* rolled_back) {
+  const or_cfg* c = &s->m->c;
+  float* logits = (float*)malloc(sizeof(float) * (size_t)c->vocab);
+  int32_t total = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    int32_t r = rows[i], p = s->pos[r], rb = 0;
+    int32_t* h = s->hist + (int64_t)r * (s->max_seq + 1);
+    for (int32_t q = s->shadow_len[r]; q < p; ++q) {
+      forward_token(s, 1, r, q, h[q], det, logits);
+      s->stats[7] += 1;
+      float v1, v2, g; int32_t i1, i2, nan = 0;
+      or_top2(logits, 1, c->vocab, &v1, &i1, &v2, &i2, &g, &nan);
+      if (nan) s->stats[8] += 1;
+      if (i1 != h[q + 1]) {      /* first disagreement: roll back to q+1 */
+        rb = p - (q + 1);
+        h[q + 1] = i1;
+        p = q + 1;
+        s->pos[r] = p;
+        s->wstats[1] += 1;
+        break;
+      }
+    }
+    s->shadow_len[r] = p;
+    s->wstats[0] += 1;
+    s->wstats[2] += (uint64_t)rb;
+    total += rb;
+    if (new_pos) new_pos[i] = p;
+    if (last_tok) last_tok[i] = h[p];
+    if (rolled_back) rolled_back[i] = rb;
+  }
+  free(logits);
+  return total;
+}
+
+void or_state_window_stats(const or_state* s, uint64_t* out3) { memcpy(out3, s->wstats, sizeof(s->wstats)); }

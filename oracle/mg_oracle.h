@@ -124,6 +124,19 @@ uint64_t or_state_digest(const or_state* s, int32_t which, int32_t skip_row, int
 /* stats: [steps, rows, protected_rows, triggers, verified, repairs, verifier_launches, catchup_tokens, nan] */
 void     or_state_stats(const or_state* s, uint64_t* out9);
 
+/* Repair-action ablation: 0 = copy the verifier column on a
+ * repair (default), 1 = token-only (leave the BF16 column). */
+void     or_state_set_repair_mode(or_state* s, int32_t mode);
+
+/* LLM-42-style windowed verification with rollback over every token
+ * committed since the row's last verification (
+ * SURVEY 8(f) NEXT-2).  See mg_oracle.c for the exact order.  Returns the
+ * number of discarded tokens. */
+int32_t  or_verify_window(or_state* s, const int32_t* rows, int32_t n, const or_sched* det,
+                          int32_t* new_pos, int32_t* last_tok, int32_t* rolled_back);
+/* [window verifies (rows), rollbacks, rolled-back tokens] */
+void     or_state_window_stats(const or_state* s, uint64_t* out3);
+
 #ifdef __cplusplus
 }
 #endif
