@@ -282,7 +282,7 @@ def run_gpu(args):
     if not args.quick and args.paper_batch > 0:
         eng.close()
         pb = args.paper_batch
-        e8 = Engine(shp, max_batch=pb, max_slots=pb, max_seq=max_seq, page_size=64)
+        e8 = Engine(shp, max_batch=pb, max_slots=pb, max_seq=ctx0 + W + max(K, 2 * args.window) + 2, page_size=64)
         cal8 = calibrate(e8, inputs.prompts(pb, ctx0, shp["vocab"], seed=1000 + rank * pb), 3, K)
         t8 = cal8["tau100"] if cal8["tau100"] is not None else math.inf
         _, (t8,) = sharding.aggregate([], [t8], device="cuda")
@@ -291,8 +291,17 @@ def run_gpu(args):
         tp = cal8["tau_p"]  # 2 max eps: the argmax-bound threshold, conservative
         r8 = {n: _decode_run(e8, ev8, t, p1, W, K, timed=True)
               for n, t in (("bf16", 0.0), ("margingate", t8), ("margingate_tau_p", tp), ("always_on", math.inf))}
+        # NEXT-3 repair-action ablation: token-only repair at tau100
+        e8.set_policy(repair_action=1)
+        r8["margingate_token_only"] = _decode_run(e8, ev8, t8, p1, W, K, timed=True)
+        # NEXT-4 global batch-invariant baseline: every row on the pinned plan, tau = 0
+        e8.set_policy(fast_schedule=1, repair_action=0)
+        r8["batch_invariant"] = _decode_run(e8, ev8, 0.0, p1, W, K, timed=True)
+        e8.set_policy(0, 0)
+        # NEXT-2 LLM-42 windowed verify + rollback, K = 64, over 2 windows
+        win = _window_run(e8, ev8, p1, W, 2 * args.window, args.window)
         e8.close()
-        paper = {"batch": pb, "tau100": t8, "calibration": cal8, "r": r8}
+        paper = {"batch": pb, "tau100": t8, "calibration": cal8, "r": r8, "window": win}
 
     # ---- aggregate over ranks (the only collectives: stats SUM, time MAX)
     def det(a, b, prot):
@@ -400,8 +409,26 @@ def run_gpu(args):
                          "increment_ratio": round(metrics.increment_ratio(inc_ao, inc_tp), 3) if inc_tp > 0.01 else None,
                          "trigger_pct": round(100 * metrics.rates(r8["margingate_tau_p"][1])["r_verify"], 3)},
             "protected_row_equals_reference": {n: r8[n][0][0] == r8["always_on"][0][0]
-                                               for n in ("bf16", "margingate", "margingate_tau_p")},
+                                               for n in ("bf16", "margingate", "margingate_tau_p",
+                                                         "margingate_token_only", "batch_invariant")},
+            "token_only_repair": {"inc": round(metrics.latency_increment(tm["margingate_token_only"], tm["bf16"]), 4),
+                                  "repairs": r8["margingate_token_only"][1]["repairs"],
+                                  "note": "repair-action ablation, PAPER.md:317"},
+            "batch_invariant": {"inc": round(metrics.latency_increment(tm["batch_invariant"], tm["bf16"]), 4),
+                                "note": "global batch-invariant fast schedule at tau=0 (PAPER.md:227)"},
             "note": "rank 0's numbers (times not reduced over ranks)"}
+        wseq, wtok, wms, wst = paper["window"]
+        t_tok_bf16 = tm["bf16"] / (pb * K)
+        inc_w = (wms / wtok) / t_tok_bf16 - 1
+        n_ref = min(len(wseq[0]), len(r8["always_on"][0][0]))
+        line["arms"]["paper_protocol"]["llm42_window"] = {
+            "window": args.window, "steps": 2 * args.window, "tok_s": round(ws * wtok / (wms * 1e-3), 2),
+            "inc": round(inc_w, 4),
+            "increment_ratio_vs_margingate": round(inc_w / inc_mg, 3) if inc_mg > 0.01 else None,
+            "net_tokens": wtok, **wst,
+            "protected_row_equals_reference_prefix": wseq[0][:n_ref] == r8["always_on"][0][0][:n_ref],
+            "note": "PAPER.md:251 LLM-42 K=64 analog: BF16 steps + windowed verify with rollback of the protected "
+                    "row; inc per net committed token vs BF16 per token"}
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, shp, tau)
     if ws > 1:
@@ -483,10 +510,13 @@ def run_reference(args):
             "e2e": {"value": round(v, 5), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
-def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False):
+def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False, flips=None):
     """Fresh prefill of `prompts`, W + K decode steps at threshold tau; eps (a
     list) collects eps_pert per (row, step) -- only valid at tau = inf with
-    every row protected, where the verifier's rank k is row k."""
+    every row protected, where the verifier's rank k is row k.  flips (a
+    list) collects (fast margin g, fast token != verifier token) per (row,
+    step) of the gated rows -- at tau = inf every step is synchronous (the
+    committed prefix is the reference's)."""
     import torch
     B = len(prompts)
     V = eng.shape["vocab"]
@@ -516,6 +546,9 @@ def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False):
         o = out.cpu().numpy()
         for b in range(B):
             seqs[b].append(int(o[b]))
+        if flips is not None:
+            r = eng.last_step(B)
+            flips.extend((float(r["g"][b]), bool(r["f_tok"][b] != r["v_tok"][b])) for b in range(B) if r["trig"][b])
         if eps is not None:
             idx = torch.topk(capv, 50, dim=1).indices          # reference top-50
             d = (capf.gather(1, idx) - capv.gather(1, idx)).abs().amax(dim=1)
@@ -532,6 +565,65 @@ def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False):
     return seqs, st, ms
 
 
+def _window_run(eng, prompts, prot, W, K, window):
+    """LLM-42-style comparator:
+    pure BF16 steps, and every `window` steps mg_verify_window on the
+    protected rows (rollback at the first disagreement).  Fresh prefill, W
+    warm-up steps (verified at their end), then K timed steps ending with a
+    verify.  Returns (verified sequences of the rows, net committed tokens in
+    the timed region, ms, window stats)."""
+    import torch
+    B = len(prompts)
+    P = [len(p) for p in prompts]
+    rows = list(range(B))
+    vrows = [i for i in rows if prot[i]]
+    for i in range(B):
+        try:
+            eng.release(i)
+        except Exception:
+            pass
+    seqs = [[eng.prefill(i, p)] for i, p in enumerate(prompts)]
+    hist = []
+
+    def flush():
+        o = torch.stack(hist).cpu().numpy() if hist else np.empty((0, B), np.int32)
+        hist.clear()
+        for b in range(B):
+            seqs[b].extend(int(t) for t in o[:, b])
+        pos, last, rb = eng.verify_window(vrows)
+        for j, b in enumerate(vrows):
+            n = int(pos[j]) - P[b] + 1
+            del seqs[b][n:]
+            seqs[b][-1] = int(last[j])
+
+    out_bufs = [torch.empty(B, dtype=torch.int32, device="cuda") for _ in range(W + K)]
+    it = iter(out_bufs)
+
+    def step_into():
+        o = next(it)
+        eng.step(rows, None, 0.0, o)
+        return o
+
+    # warm-up: W steps then a verify
+    for _ in range(W):
+        hist.append(step_into())
+    flush()
+    n0 = sum(len(s) for s in seqs)
+    s0 = eng.stats()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(eng.stream)
+    for k in range(K):
+        hist.append(step_into())
+        if (k + 1) % window == 0 or k == K - 1:
+            flush()
+    e1.record(eng.stream)
+    torch.cuda.synchronize()
+    s1 = eng.stats()
+    st = {k: s1[k] - s0[k] for k in ("window_rows", "rollbacks", "rolled_back_tokens", "catchup_tokens")}
+    return seqs, sum(len(s) for s in seqs) - n0, e0.elapsed_time(e1), st
+
+
 def calibrate(eng, prompts, W, K):
     """SURVEY A22 / PAPER.md:260-265, 402: eps_pert on calibration prompts
     (tau = inf, all rows protected: batched fast vs deterministic verifier
@@ -541,10 +633,11 @@ def calibrate(eng, prompts, W, K):
     from paper_2605_30218_b200 import inputs, metrics
     B = len(prompts)
     prot = inputs.protected_mask(B, "all")
-    eps = []
-    ref, _, _ = _decode_run(eng, prompts, math.inf, prot, W, K, eps=eps)
+    eps, fl = [], []
+    ref, _, _ = _decode_run(eng, prompts, math.inf, prot, W, K, eps=eps, flips=fl)
     tau_p = metrics.pert_tau(eps)
     grid = sorted(set([0.0] + [tau_p * 2.0 ** k for k in range(-3, 4)]))
+    ev = [g for g, f in fl if f]
     rows = []
     for tau in grid:
         seqs, st, _ = _decode_run(eng, prompts, tau, prot, W, K)
@@ -552,7 +645,10 @@ def calibrate(eng, prompts, W, K):
                      "trigger_pct": round(100 * metrics.rates(st)["r_verify"], 3)})
     t100 = metrics.tau100([(r["tau"], r["det_pct"] / 100) for r in rows])
     return {"eps_pert_max": max(eps), "eps_pert_p50": float(np.median(eps)), "samples": len(eps),
-            "tau_p": tau_p, "grid": rows, "tau100": t100}
+            "tau_p": tau_p, "grid": rows, "tau100": t100,
+            # synchronous flip rate and trigger recall (tab:hetero)
+            "sync_flip_rate": len(ev) / len(fl) if fl else None, "flip_events": len(ev),
+            "recall": {f"{t:.4g}": metrics.margin_recall(ev, t) for t in grid if t > 0} if ev else None}
 
 
 def run_sweep(args):
@@ -588,7 +684,25 @@ def run_sweep(args):
                                 for n in ("bf16", "margingate")},
         }
     eng.close()
+    # NEXT-3 (App. C tab:hetero): trigger check on same-prompt-replicated
+    # (homogeneous) vs mixed prompts of ragged lengths (heterogeneous; per-row
+    # positions, the paged cache needs no padding)
+    het = {}
+    eng = Engine(shp, max_batch=B, max_slots=B, max_seq=prompt_len * 3 // 2 + W + K + 4, page_size=64)
+    homo_p = inputs.prompts(1, prompt_len, shp["vocab"], seed=2000) * B
+    lens = inputs.ragged_lengths(B, prompt_len // 2, prompt_len * 3 // 2, seed=2001)
+    het_p = inputs.prompts(B, lens, shp["vocab"], seed=3000)
+    for name, ps in (("homogeneous", homo_p), ("heterogeneous", het_p)):
+        fl = []
+        _decode_run(eng, ps, math.inf, inputs.protected_mask(B, "all"), W, K, flips=fl)
+        ev = [g for g, f in fl if f]
+        het[name] = {"sync_flip_rate": round(len(ev) / len(fl), 5), "flip_events": len(ev), "samples": len(fl),
+                     "recall": {f"{t:.4g}": metrics.margin_recall(ev, t)
+                                for t in (cal["tau_p"] / 2, cal["tau_p"], 2 * cal["tau_p"]) if t > 0} if ev else None}
+    het["lengths"] = lens
+    eng.close()
     return {"metric": "tau calibration sweep (SURVEY 8(f) NEXT-1, A22)", "model": args.model,
+            "hetero_check": het,
             "workload": f"{args.workload}-shaped prompt {prompt_len}, {K} timed decode steps after {W}, batch {B}",
             "calibration": {"seeds": "1000 + i", **cal},
             "evaluation": {"seeds": "7 + i", **evals},
@@ -610,6 +724,7 @@ def main():
     ap.add_argument("--quick", action="store_true", help="skip the other protection mode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--paper-batch", type=int, default=8, help="batch of the paper-protocol arm (0: off)")
+    ap.add_argument("--window", type=int, default=64, help="LLM-42 verify window (PAPER.md:251 K=64)")
     ap.add_argument("--sweep", action="store_true", help="tau calibration sweep report (NEXT-1) instead of the "
                                                           "bench line")
     args = ap.parse_args()

@@ -74,8 +74,27 @@ typedef struct {
  * (PAPER.md:215). */
 typedef struct {
   uint64_t steps, rows, protected_rows, triggers, verified, repairs, verifier_launches, catchup_tokens;
+  /* windowed verification (mg_verify_window): rows verified, rows rolled
+   * back, committed tokens discarded by rollbacks */
+  uint64_t window_rows, rollbacks, rolled_back_tokens;
   uint32_t error_flags; /* bit0: NaN logit seen */
 } mg_stats_t;
+
+/* Fast-path schedule (mg_set_policy).
+ *   MG_FAST_BATCH_SHAPED     the performance-chosen plan sched_fast(B) whose
+ *                            attention splits depend on the batch -- the
+ *                            paper's source of batch variance;
+ *                            default.
+ *   MG_FAST_BATCH_INVARIANT  every row runs the verifier's pinned schedule:
+ *                            the "global intervention" baseline of PAPER.md:227
+ *                            (Batch-Invariant Ops). */
+typedef enum { MG_FAST_BATCH_SHAPED = 0, MG_FAST_BATCH_INVARIANT = 1 } mg_fast_schedule;
+/* Repair action on a verifier disagreement (mg_set_policy).
+ *   MG_REPAIR_COLUMN      emit the verifier token AND copy the verifier's K/V
+ *                         column p into the fast cache; default.
+ *   MG_REPAIR_TOKEN_ONLY  emit the verifier token, keep the tentative BF16
+ *                         column: the ablation of PAPER.md:317. */
+typedef enum { MG_REPAIR_COLUMN = 0, MG_REPAIR_TOKEN_ONLY = 1 } mg_repair_action;
 
 /* Sizes the four buffers for `cfg`.  MG_ERR_INVALID on unsupported shapes
  * (d_model % 64, d_ff % 64, (H+2KV)*hd % 128, vocab % 128, head_dim in
@@ -111,6 +130,29 @@ mg_status mg_prefill(mg_ctx* ctx, int32_t slot, const int32_t* prompt_host, int3
  * max_seq. */
 mg_status mg_decode_step(mg_ctx* ctx, const int32_t* slots_host, int32_t batch, const uint8_t* protected_host,
                          float threshold, int32_t* tokens_out_dev, uint8_t* kind_out_dev, float* margin_out_dev);
+
+/* Selects the fast-path schedule and the repair action for later steps
+ * (values of mg_fast_schedule / mg_repair_action).  MG_ERR_INVALID for
+ * unknown values (no state change). */
+mg_status mg_set_policy(mg_ctx* ctx, int32_t fast_schedule, int32_t repair_action);
+
+/* LLM-42-style windowed verification with rollback ("keeps the
+ * default path but verifies every token", "verifier setting
+ * K=64", "restart-from-rollback").  For each
+ * of the n active, distinct slots in slots_host, every token committed since
+ * the slot's last verification (positions shadow_len+1 .. p) is checked in
+ * order against the deterministic verifier run over the committed prefix
+ * (the pinned schedule, shadow cache, reading A1).  At the first disagreement
+ * at position m the slot ROLLS BACK: the verifier token replaces the token at
+ * m, the tokens after m are discarded, and the next decode step consumes
+ * position m.  Outputs (host, nullable, n entries): pos_host = the position
+ * of the slot's last committed token after the call, last_token_host = that
+ * token, rolled_back_host = tokens discarded.  Synchronises.  Cost: one
+ * verifier forward over all unverified tokens of the n slots (chunks of
+ * verify_chunk tokens) with the LM head on every one.  MG_ERR_INVALID for
+ * n not in [1, max_batch] or an inactive / duplicate slot. */
+mg_status mg_verify_window(mg_ctx* ctx, const int32_t* slots_host, int32_t n, int32_t* pos_host,
+                           int32_t* last_token_host, int32_t* rolled_back_host);
 
 /* Synchronises the stream and copies the counters; returns MG_ERR_NUMERIC if
  * a NaN logit was seen (counters still written). */

@@ -48,12 +48,13 @@ class MgBuffers(C.Structure):
 class MgStats(C.Structure):
     _fields_ = [("steps", C.c_uint64), ("rows", C.c_uint64), ("protected_rows", C.c_uint64),
                 ("triggers", C.c_uint64), ("verified", C.c_uint64), ("repairs", C.c_uint64),
-                ("verifier_launches", C.c_uint64), ("catchup_tokens", C.c_uint64), ("error_flags", C.c_uint32)]
+                ("verifier_launches", C.c_uint64), ("catchup_tokens", C.c_uint64), ("window_rows", C.c_uint64),
+                ("rollbacks", C.c_uint64), ("rolled_back_tokens", C.c_uint64), ("error_flags", C.c_uint32)]
 
 
 # every symbol declared in include/mg.h and include/mg_debug.h
 PUBLIC_SYMBOLS = ["mg_query_sizes", "mg_init", "mg_prefill", "mg_decode_step", "mg_stats", "mg_release",
-                  "mg_destroy", "mg_last_error"]
+                  "mg_destroy", "mg_last_error", "mg_set_policy", "mg_verify_window"]
 DEBUG_SYMBOLS = ["mgd_gen_tensor", "mgd_rmsnorm", "mgd_gemm", "mgd_qkv_epilogue", "mgd_attention", "mgd_residual",
                  "mgd_swiglu", "mgd_top2", "mgd_gate", "mgd_read_column", "mgd_cache_digest", "mgd_last_step",
                  "mgd_capture_logits", "mgd_weight", "mgd_schedule", "mgd_launch_count", "mgd_set_timing",
@@ -68,6 +69,8 @@ _SIGS = {
     "mg_prefill": [_vp, _i32, _P(_i32), _i32, _P(_i32)],
     "mg_decode_step": [_vp, _P(_i32), _i32, _P(C.c_uint8), _f32, _vp, _vp, _vp],
     "mg_stats": [_vp, _P(MgStats)],
+    "mg_set_policy": [_vp, _i32, _i32],
+    "mg_verify_window": [_vp, _vp, _i32, _vp, _vp, _vp],
     "mg_release": [_vp, _i32],
     "mg_destroy": [_vp],
     "mg_last_error": [_vp],

@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
   const int f = a.f_tok[b];
   const int v = tr ? a.v_tok[a.rank[b]] : -1;
   const int kind = !tr ? 0 : (v == f ? 1 : 2);
-  if (kind == 2) copy_cols(a.copy, slot, p, p + 1, threadIdx.x, blockDim.x);  // single-column repair
+  if (kind == 2 && a.repair_copy) copy_cols(a.copy, slot, p, p + 1, threadIdx.x, blockDim.x);  // single-column repair
   if (threadIdx.x == 0) {
     const int out = kind == 2 ? v : f;
     a.tokens_out[b] = out;
@@ -280,6 +280,67 @@ __global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
 
 cudaError_t launch_commit(const CommitArgs& a, cudaStream_t st) {
   return launch_k(k_commit, dim3(a.B), dim3(256), 0, st, a);
+}
+
+// ------------------------------------------------------------------ window verify
+// LLM-42-style windowed verification (include/mg.h
+// mg_verify_window).  Row i's unverified tokens are the inputs at positions
+// shadow_len .. p-1; the verifier's argmax at q predicts position q+1.
+// k_window_list: catch-up list entries off[i] + (q - shadow_len).  CTA per row.
+__global__ void k_window_list(WindowArgs a) {
+  griddep();
+  const int i = blockIdx.x;
+  const int slot = a.slots[i], s0 = a.shadow_len[slot], p = a.pos[slot];
+  const int32_t* h = a.hist + (size_t)slot * a.hist_stride;
+  for (int q = s0 + threadIdx.x; q < p; q += blockDim.x) {
+    const int e = a.off[i] + (q - s0);
+    a.cu_slot[e] = slot;
+    a.cu_pos[e] = q;
+    a.cu_tok[e] = h[q];
+    a.cu_nk[e] = q + 1;
+  }
+}
+
+cudaError_t launch_window_list(const WindowArgs& a, cudaStream_t st) {
+  return launch_k(k_window_list, dim3(a.n), dim3(128), 0, st, a);
+}
+
+// k_window_commit: first disagreement m -> hist[m] = verifier token,
+// pos = shadow_len = m (rollback); else shadow_len = p.  CTA (one warp) per row;
+// the first mismatch is the minimum mismatching q over a warp-strided scan.
+__global__ void k_window_commit(WindowArgs a) {
+  griddep();
+  const int i = blockIdx.x, lane = threadIdx.x;
+  const int slot = a.slots[i], s0 = a.shadow_len[slot], p = a.pos[slot];
+  int32_t* h = a.hist + (size_t)slot * a.hist_stride;
+  int first = INT_MAX;
+  for (int q = s0 + lane; q < p; q += 32)
+    if (a.v_tok[a.off[i] + (q - s0)] != h[q + 1]) { first = q; break; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+  if (lane != 0) return;
+  int np = p, rb = 0;
+  if (first != INT_MAX) {
+    np = first + 1;
+    rb = p - np;
+    h[np] = a.v_tok[a.off[i] + (first - s0)];
+    a.pos[slot] = np;
+  }
+  a.shadow_len[slot] = np;
+  a.res[3 * i] = np;
+  a.res[3 * i + 1] = h[np];
+  a.res[3 * i + 2] = rb;
+  unsigned long long* s = a.stats;
+  atomicAdd(&s[8], 1ull);
+  atomicAdd(&s[7], (unsigned long long)(p - s0));
+  if (first != INT_MAX) {
+    atomicAdd(&s[9], 1ull);
+    atomicAdd(&s[10], (unsigned long long)rb);
+  }
+}
+
+cudaError_t launch_window_commit(const WindowArgs& a, cudaStream_t st) {
+  return launch_k(k_window_commit, dim3(a.n), dim3(32), 0, st, a);
 }
 
 // prefill bookkeeping: hist[slot][len] = token, pos = shadow_len = len

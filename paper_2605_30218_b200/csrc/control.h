@@ -51,6 +51,7 @@ struct CommitArgs {
   int32_t* hist;
   int hist_stride;
   ColCopy copy;            // shadow -> fast
+  int repair_copy;         // 1: copy the verifier column on a repair; 0: token-only
   int32_t* tokens_out;
   uint8_t* kind_out;
   float* margin_out;
@@ -63,6 +64,26 @@ struct CommitArgs {
   int32_t* dbg_out;
 };
 cudaError_t launch_commit(const CommitArgs& a, cudaStream_t st);
+
+// windowed verification (LLM-42 style)
+struct WindowArgs {
+  int n;
+  const int32_t* slots;    // [n]
+  const int32_t* off;      // [n] catch-up list offset of each row
+  int32_t* pos;            // [max_slots]
+  int32_t* shadow_len;
+  int32_t* hist;
+  int hist_stride;
+  int32_t* cu_slot;        // catch-up list (k_window_list writes it)
+  int32_t* cu_pos;
+  int32_t* cu_tok;
+  int32_t* cu_nk;
+  const int32_t* v_tok;    // [M] verifier argmax of every catch-up token
+  int32_t* res;            // [3n]: new pos, last token, rolled-back count
+  unsigned long long* stats;
+};
+cudaError_t launch_window_list(const WindowArgs& a, cudaStream_t st);
+cudaError_t launch_window_commit(const WindowArgs& a, cudaStream_t st);
 
 cudaError_t launch_prepare(const int32_t* slots, int B, const int32_t* pos, const int32_t* hist, int hist_stride,
                            int32_t* f_slot, int32_t* f_pos, int32_t* f_tok, int32_t* f_nk, cudaStream_t st);

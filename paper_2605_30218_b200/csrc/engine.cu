@@ -150,7 +150,15 @@ OpSched op_lm(int N, int K, int T, bool det) {  // LM head: no split (top-2 read
 
 }  // namespace
 
+static Sched sched_det(const mg_ctx* c, int T, int max_ctx);
+
 static Sched sched_fast(const mg_ctx* c, int T, int max_ctx) {
+  if (c->fast_mode == MG_FAST_BATCH_INVARIANT) {
+    // global batch-invariant baseline (NEXT-4): the verifier's
+    // pinned plan for every row; splits sized from the capacity (one graph)
+    Sched s = sched_det(c, T, c->cfg.max_seq);
+    return s;
+  }
   Sched s;
   s.qkv = op_fast(c->NQKV, c->d, T);
   s.o = op_fast(c->d, c->NQ, T);
@@ -265,7 +273,7 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   c->xg = s.take<uint16_t>((size_t)B * c->d);
   c->xgn = s.take<uint16_t>((size_t)B * c->d);
   c->part = s.take<float>(c->part_elems);
-  c->logits = s.take<float>((size_t)B * c->V);
+  c->logits = s.take<float>((size_t)Tm * c->V);  // window verify: LM head over whole chunks
   c->attn_acc = s.take<float>(attn_rows * c->hd);
   c->attn_ml = s.take<float>(attn_rows * 2);
   c->attn_cnt = s.take<int32_t>((size_t)Tm * c->KV);
@@ -293,6 +301,8 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   c->cu_tok = s.take<int32_t>(cu); c->cu_nk = s.take<int32_t>(cu);
   c->v_tok = s.take<int32_t>(B); c->v_i2 = s.take<int32_t>(B);
   c->v_g = s.take<float>(B); c->v_v1 = s.take<float>(B); c->v_v2 = s.take<float>(B);
+  c->w_tok = s.take<int32_t>(cu);
+  c->w_res = s.take<int32_t>(3 * (size_t)B);
   {
     const size_t a4 = 4 * (size_t)B, b2 = 2 * (size_t)c->max_pages;
     c->staging_d = s.take<int32_t>((a4 > b2 ? a4 : b2) + 64);
@@ -943,6 +953,7 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
   ca.rank = c->rank_d; ca.ctrl = c->ctrl_d; ca.f_tok = c->f_tok; ca.g = c->f_g; ca.v_tok = c->v_tok; ca.v_g = c->v_g;
   ca.pos = c->pos_d; ca.shadow_len = c->shadow_d; ca.hist = c->hist_d; ca.hist_stride = c->cfg.max_seq + 1;
   ca.copy = col_copy(c, true);
+  ca.repair_copy = c->repair_mode == MG_REPAIR_COLUMN ? 1 : 0;
   ca.tokens_out = tokens_out; ca.kind_out = kind_out; ca.margin_out = margin_out; ca.stats = c->stats_d;
   ca.dbg_vtok = c->dbg_vtok; ca.dbg_vg = c->dbg_vg; ca.dbg_kind = c->dbg_kind; ca.dbg_trig = c->dbg_trig;
   ca.dbg_out = c->dbg_out;
@@ -964,6 +975,86 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
   return MG_OK;
 }
 
+mg_status mg_set_policy(mg_ctx* c, int32_t fast_schedule, int32_t repair_action) {
+  if (!c) return MG_ERR_INVALID;
+  if (c->dead) return fail(c, MG_ERR_CUDA, "context is dead: " + c->err);
+  if (fast_schedule != MG_FAST_BATCH_SHAPED && fast_schedule != MG_FAST_BATCH_INVARIANT)
+    return fail(c, MG_ERR_INVALID, "unknown fast schedule");
+  if (repair_action != MG_REPAIR_COLUMN && repair_action != MG_REPAIR_TOKEN_ONLY)
+    return fail(c, MG_ERR_INVALID, "unknown repair action");
+  c->fast_mode = fast_schedule;
+  c->repair_mode = repair_action;
+  return MG_OK;
+}
+
+// LLM-42-style windowed verification with rollback (include/mg.h).
+mg_status mg_verify_window(mg_ctx* c, const int32_t* slots, int32_t n, int32_t* pos_out, int32_t* last_out,
+                           int32_t* rb_out) {
+  if (!c) return MG_ERR_INVALID;
+  if (c->dead) return fail(c, MG_ERR_CUDA, "context is dead: " + c->err);
+  if (!slots || n < 1 || n > c->cfg.max_batch) return fail(c, MG_ERR_INVALID, "bad window batch");
+  std::vector<char> seen(c->cfg.max_slots, 0);
+  for (int i = 0; i < n; ++i) {
+    const int s = slots[i];
+    if (s < 0 || s >= c->cfg.max_slots || !c->active[s] || seen[s])
+      return fail(c, MG_ERR_INVALID, "inactive or duplicate slot");
+    seen[s] = 1;
+  }
+  // host-side catch-up list offsets (mirrors of pos / shadow_len)
+  std::vector<int32_t> w(2 * n);
+  int M = 0, vmax = 1;
+  for (int i = 0; i < n; ++i) {
+    const int s = slots[i];
+    w[i] = s;
+    w[n + i] = M;
+    M += c->pos_h[s] - c->shadow_h[s];
+    if (c->pos_h[s] > vmax) vmax = c->pos_h[s];
+  }
+  mg_status r = upload(c, w);
+  if (r) return r;
+  WindowArgs wa{};
+  wa.n = n; wa.slots = c->staging_d; wa.off = c->staging_d + n;
+  wa.pos = c->pos_d; wa.shadow_len = c->shadow_d; wa.hist = c->hist_d; wa.hist_stride = c->cfg.max_seq + 1;
+  wa.cu_slot = c->cu_slot; wa.cu_pos = c->cu_pos; wa.cu_tok = c->cu_tok; wa.cu_nk = c->cu_nk;
+  wa.v_tok = c->w_tok; wa.res = c->w_res; wa.stats = c->stats_d;
+  if (M > 0) {
+    CK(launch_window_list(wa, c->st));
+    c->launches++;
+    // the deterministic forward over the unverified tokens, LM head + argmax on
+    // every one of them (the same pinned schedule as the per-step verifier)
+    for (int c0 = 0; c0 < M; c0 += c->Tv) {
+      const int T = M - c0 < c->Tv ? M - c0 : c->Tv;
+      Sched sc = sched_det(c, T, vmax);
+      r = graphed(c, std::make_tuple(2, T, sc.attn_ns, c0, 0, 0), [&]() -> mg_status {
+        mg_status rr = forward(c, T, c->cu_slot + c0, c->cu_pos + c0, c->cu_tok + c0, c->cu_nk + c0, 1, sc);
+        if (rr) return rr;
+        return lm_head(c, c->xn, c->Tmax, T, sc.lm, nullptr, c->w_tok + c0, nullptr, nullptr, nullptr);
+      });
+      if (r) return r;
+    }
+  }
+  CK(launch_window_commit(wa, c->st));
+  c->launches++;
+  int32_t* res_h = c->pinned + (c->pinned_words - (2 + c->cfg.max_batch));
+  // the ctrl region holds 2 + max_batch words; results need 3n: copy in pieces
+  std::vector<int32_t> res(3 * (size_t)n);
+  for (int i0 = 0; i0 < 3 * n; i0 += 2 + c->cfg.max_batch) {
+    const int k = 3 * n - i0 < 2 + c->cfg.max_batch ? 3 * n - i0 : 2 + c->cfg.max_batch;
+    CK(cudaMemcpyAsync(res_h, c->w_res + i0, (size_t)k * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    memcpy(res.data() + i0, res_h, (size_t)k * 4);
+  }
+  for (int i = 0; i < n; ++i) {
+    const int s = slots[i];
+    c->pos_h[s] = res[3 * i];
+    c->shadow_h[s] = res[3 * i];
+    if (pos_out) pos_out[i] = res[3 * i];
+    if (last_out) last_out[i] = res[3 * i + 1];
+    if (rb_out) rb_out[i] = res[3 * i + 2];
+  }
+  return MG_OK;
+}
+
 mg_status mg_stats(mg_ctx* c, mg_stats_t* out) {
   if (!c || !out) return MG_ERR_INVALID;
   if (c->dead) return fail(c, MG_ERR_CUDA, "context is dead: " + c->err);
@@ -976,6 +1067,7 @@ mg_status mg_stats(mg_ctx* c, mg_stats_t* out) {
   if (flags[1]) return fail(c, MG_ERR_CUDA, "a layer-chain grid barrier timed out: results are invalid");
   out->steps = s[0]; out->rows = s[1]; out->protected_rows = s[2]; out->triggers = s[3];
   out->verified = s[4]; out->repairs = s[5]; out->verifier_launches = s[6]; out->catchup_tokens = s[7];
+  out->window_rows = s[8]; out->rollbacks = s[9]; out->rolled_back_tokens = s[10];
   out->error_flags = nan ? 1u : 0u;
   return nan ? MG_ERR_NUMERIC : MG_OK;
 }

@@ -82,6 +82,8 @@ struct mg_ctx {
   int chain_trace_layer = -2;
   int chain_pf = 0;
   int fast_sk_override = 0;  // MG_FAST_SK (measurement)
+  int fast_mode = 0;         // mg_fast_schedule (mg_set_policy)
+  int repair_mode = 0;       // mg_repair_action
   int det_sk = 512;          // verifier attention keys per split (A14; MG_DET_SK for measurement)  // chain L2 run-ahead (k-blocks per CTA; measured harmful, off)
   CUtensorMap attn_qmap, kv_map[2];      // TMA maps: q [Tmax][H][hd]; pools (fast, shadow)
   float *rope_cos, *rope_sin;
@@ -98,6 +100,7 @@ struct mg_ctx {
   int32_t *rank_d, *ctrl_d, *last_d;
   int32_t *cu_slot, *cu_pos, *cu_tok, *cu_nk;
   int32_t *v_tok, *v_i2;
+  int32_t *w_tok, *w_res;  // window verify: argmax per catch-up token [B*max_seq]; results [3B]
   float *v_g, *v_v1, *v_v2;
   int32_t* staging_d;  // uploads: [slots | prot bytes | pt updates]
   // debug record

@@ -13,6 +13,8 @@ from . import _lib
 from ._lib import MgBuffers, MgConfig, MgSizes, MgStats, check, lib
 
 KIND_FAST, KIND_VERIFIED, KIND_REPAIR = 0, 1, 2
+FAST_BATCH_SHAPED, FAST_BATCH_INVARIANT = 0, 1   # mg_fast_schedule
+REPAIR_COLUMN, REPAIR_TOKEN_ONLY = 0, 1         # mg_repair_action
 
 
 def make_config(shape: dict, max_batch: int, max_slots: int, max_seq: int, page_size: int = 64,
@@ -80,6 +82,22 @@ class Engine:
         d = {k: int(getattr(s, k)) for k, _ in MgStats._fields_}
         d["nan"] = st == _lib.MG_ERR_NUMERIC
         return d
+
+    def set_policy(self, fast_schedule: int = 0, repair_action: int = 0):
+        """mg_set_policy: fast_schedule 0 batch-shaped (default) / 1 batch-invariant
+        (PAPER.md:227 global baseline); repair_action 0 column /
+        1 token-only ablation."""
+        check(lib().mg_set_policy(self.ctx, int(fast_schedule), int(repair_action)), self.ctx, "mg_set_policy")
+
+    def verify_window(self, slots):
+        """mg_verify_window (LLM-42-style verify + rollback, PAPER.md:227, 251,
+        255).  Returns (pos, last_token, rolled_back) numpy arrays per slot."""
+        s = np.ascontiguousarray(slots, dtype=np.int32)
+        n = s.size
+        pos, last, rb = np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n, np.int32)
+        check(lib().mg_verify_window(self.ctx, s.ctypes.data, n, pos.ctypes.data, last.ctypes.data, rb.ctypes.data),
+              self.ctx, "mg_verify_window")
+        return pos, last, rb
 
     def release(self, slot: int):
         check(lib().mg_release(self.ctx, slot), self.ctx, "mg_release")
