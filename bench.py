@@ -179,20 +179,24 @@ def run_gpu(args):
     keys = ["steps", "rows", "protected_rows", "triggers", "verified", "repairs", "verifier_launches",
             "catchup_tokens"]
 
-    def run_arm(tau, prot, timing=False, clocks=None):
+    def run_arm(tau, prot, timing=False, clocks=None, pipelined=False):
         """Fresh deterministic prefill, W warm-up steps, K timed steps (CUDA events
-        on the engine's stream, barrier + synchronize on both sides)."""
+        on the engine's stream, barrier + synchronize on both sides).
+        pipelined: MG_VERIFY_PIPELINED (include/mg.h) -- a gated row's
+        verifier rides on its next step; tokens = emitted minus replaced (kind 4)."""
         for i in range(B):
             try:
                 eng.release(i)
             except Exception:
                 pass
+        eng.set_policy(verify_mode=1 if pipelined else 0)
         first = [eng.prefill(i, p) for i, p in enumerate(prompts)]
         s0 = eng.stats()
-        toks = []
+        toks, kinds_w = [], []
         for _ in range(W):
             eng.step(list(range(B)), prot, tau, out, kind)
             toks.append(out.cpu().numpy().copy())
+            kinds_w.append(kind.cpu().numpy().copy())
         eng.set_timing(timing)
         if clocks:
             clocks.start()
@@ -202,12 +206,13 @@ def run_gpu(args):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         outs = torch.empty((K, B), dtype=torch.int32, device="cuda")
+        kinds = torch.empty((K, B), dtype=torch.uint8, device="cuda")
         prof = clocks is not None and os.environ.get("MG_PROFILE_TIMED") == "1"  # ncu --profile-from-start off
         if prof:
             torch.cuda.profiler.start()
         e0.record(stream)
         for k in range(K):
-            eng.step(list(range(B)), prot, tau, outs[k], kind)
+            eng.step(list(range(B)), prot, tau, outs[k], kinds[k])
         e1.record(stream)
         if prof:
             torch.cuda.synchronize()
@@ -222,8 +227,25 @@ def run_gpu(args):
         if clocks:
             r["clk"] = clocks.stop()
         s1 = eng.stats()
+        kt = kinds.cpu().numpy()
         toks += list(outs.cpu().numpy())
-        r["seqs"] = [[first[b]] + [int(t[b]) for t in toks] for b in range(B)]
+        kall = kinds_w + list(kt)
+        seqs = [[first[b]] for b in range(B)]
+        for t, kk in zip(toks, kall):
+            for b in range(B):
+                if pipelined and kk[b] == 4:
+                    seqs[b][-1] = int(t[b])
+                else:
+                    seqs[b].append(int(t[b]))
+        if pipelined:  # resolve the last tentative tokens (untimed)
+            pos, last, _ = eng.verify_window(list(range(B)))
+            for b in range(B):
+                n = int(pos[b]) - len(prompts[b]) + 1
+                del seqs[b][n:]
+                seqs[b][-1] = int(last[b])
+            eng.set_policy(verify_mode=0)
+        r["seqs"] = seqs
+        r["tokens"] = int(B * K - (kt == 4).sum()) if pipelined else B * K
         r["stats"] = {k: s1[k] - s0[k] for k in keys}
         return r
 
@@ -241,11 +263,15 @@ def run_gpu(args):
     res = {"bf16": run_arm(0.0, None)}
     res["mg"] = run_arm(tau, head, clocks=Clocks(local))
     res["ao"] = run_arm(math.inf, head)
+    # pipelined verification (include/mg.h MG_VERIFY_PIPELINED): always-on with the
+    # verifier riding on the next step's weight pass
+    res["ao_pipe"] = run_arm(math.inf, head, pipelined=True)
     other = "all" if args.protected == "one" else "one"
     if not args.quick:
         po = prot_all if other == "all" else prot_one
         res["mg_other"] = run_arm(tau, po)
         res["ao_other"] = run_arm(math.inf, po)
+        res["ao_pipe_other"] = run_arm(math.inf, po, pipelined=True)
     # dominant-kernel timing pass: the fast path with CUDA events around every
     # GEMM / attention launch (events break the PDL overlap, so this pass is
     # separate from the timed arms; the per-launch durations are what ncu's
@@ -297,7 +323,10 @@ def run_gpu(args):
         # NEXT-4 global batch-invariant baseline: every row on the pinned plan, tau = 0
         e8.set_policy(fast_schedule=1, repair_action=0)
         r8["batch_invariant"] = _decode_run(e8, ev8, 0.0, p1, W, K, timed=True)
-        e8.set_policy(0, 0)
+        e8.set_policy(0, 0, 0)
+        # pipelined verification (include/mg.h MG_VERIFY_PIPELINED)
+        r8["margingate_pipelined"] = _decode_run(e8, ev8, t8, p1, W, K, timed=True, pipelined=True)
+        r8["always_on_pipelined"] = _decode_run(e8, ev8, math.inf, p1, W, K, timed=True, pipelined=True)
         # NEXT-2 LLM-42 windowed verify + rollback, K = 64, over 2 windows
         win = _window_run(e8, ev8, p1, W, 2 * args.window, args.window)
         e8.close()
@@ -307,13 +336,22 @@ def run_gpu(args):
     def det(a, b, prot):
         return sum(1 for i in range(B) if prot[i] and res[a]["seqs"][i] == res[b]["seqs"][i]), int(prot.sum())
 
-    arms = [a for a in ("bf16", "mg", "ao", "mg_other", "ao_other") if a in res]
+    arms = [a for a in ("bf16", "mg", "ao", "ao_pipe", "mg_other", "ao_other", "ao_pipe_other") if a in res]
     vec = []
     for a in arms:
         vec += [res[a]["stats"][k] for k in keys]
+    def det_prefix(a, b, prot):  # pipelined rows may be shorter (a repair costs a step): common prefix
+        ok = 0
+        for i in range(B):
+            if prot[i]:
+                n = min(len(res[a]["seqs"][i]), len(res[b]["seqs"][i]))
+                ok += res[a]["seqs"][i][:n] == res[b]["seqs"][i][:n]
+        return ok, int(prot.sum())
+
     dh = det("mg", "ao", head)
     do = det("mg_other", "ao_other", prot_all if other == "all" else prot_one) if "mg_other" in res else (0, 0)
-    vec += [*dh, *do]
+    dp = det_prefix("ao_pipe", "ao", head)
+    vec += [*dh, *do, *dp, *[res[a]["tokens"] for a in arms]]
     times = [res[a]["ms"] for a in arms] + [e2e_ms]
     vec, times = sharding.aggregate(vec, times, device="cuda")
     if rank != 0:
@@ -321,7 +359,8 @@ def run_gpu(args):
             dist.destroy_process_group()
         return None
     stats = {a: dict(zip(keys, vec[i * len(keys):(i + 1) * len(keys)])) for i, a in enumerate(arms)}
-    dh, do = vec[len(arms) * len(keys):][:2], vec[len(arms) * len(keys):][2:4]
+    dh, do, dp = vec[len(arms) * len(keys):][:2], vec[len(arms) * len(keys):][2:4], vec[len(arms) * len(keys):][4:6]
+    ntok = dict(zip(arms, vec[len(arms) * len(keys) + 6:]))
     T = dict(zip(arms, times[:-1]))
     t_e2e = times[-1]
     tok = ws * B * K
@@ -350,13 +389,23 @@ def run_gpu(args):
         traffic = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json"))).get("bytes_per_launch")
     except Exception:
         pass
+    def pipe(a, prot_name, d):
+        inc = (T[a] / ntok[a]) / (T["bf16"] / ntok["bf16"]) - 1
+        return {"protected": prot_name, "always_on_tok_s": round(ntok[a] / (T[a] * 1e-3), 2),
+                "inc_always_on": round(inc, 4), "repairs": stats[a]["repairs"],
+                "determinism_pct": round(100 * d[0] / d[1], 2) if d and d[1] else None,
+                "note": "MG_VERIFY_PIPELINED: the verifier of step t rides on step t+1's weight pass "
+                        "(tokens = emitted - replaced); determinism = common prefix equal to the sync always-on run"}
+
     arms_out = {"bf16_tok_s": round(tok / (T["bf16"] * 1e-3), 2), "tau": tau,
                 "tau_source": "calibrated tau100 (seeds 1000 + i)" if calib else "--tau",
                 "headline": summary("mg", "ao", dh, args.protected)}
     if calib:
         arms_out["calibration"] = calib
+    arms_out["headline"]["pipelined"] = pipe("ao_pipe", args.protected, dp)
     if "mg_other" in res:
         arms_out["other"] = summary("mg_other", "ao_other", do, other)
+        arms_out["other"]["pipelined"] = pipe("ao_pipe_other", other, None)
     arms_out["paper_context"] = ("A6000, bs=8, one protected request: 2.23x (8B) / 1.99x (14B) increment reduction "
                                  "at 18.56% / 15.05% triggers (PAPER.md:5, 285, 296) -- context, not the target")
     line = {
@@ -401,7 +450,7 @@ def run_gpu(args):
         line["arms"]["paper_protocol"] = {
             "batch": pb, "protected": "one", "tau": paper["tau100"], "tau_source": "calibrated tau100",
             "eps_pert_max": paper["calibration"]["eps_pert_max"], "tau_p": paper["calibration"]["tau_p"],
-            "tok_s": {n: round(ws * pb * K / (t * 1e-3), 2) for n, t in tm.items()},
+            "tok_s": {n: round(ws * r8[n][1]["tokens"] / (t * 1e-3), 2) for n, t in tm.items()},
             "inc_margingate": round(inc_mg, 4), "inc_always_on": round(inc_ao, 4),
             "increment_ratio": round(metrics.increment_ratio(inc_ao, inc_mg), 3) if inc_mg > 0.01 else None,
             "trigger_pct": round(100 * metrics.rates(r8["margingate"][1])["r_verify"], 3),
@@ -416,6 +465,13 @@ def run_gpu(args):
                                   "note": "repair-action ablation, PAPER.md:317"},
             "batch_invariant": {"inc": round(metrics.latency_increment(tm["batch_invariant"], tm["bf16"]), 4),
                                 "note": "global batch-invariant fast schedule at tau=0 (PAPER.md:227)"},
+            "pipelined": {n: {"inc": round((tm[n] / r8[n][1]["tokens"]) / (tm["bf16"] / (pb * K)) - 1, 4),
+                              "trigger_pct": round(100 * metrics.rates(r8[n][1])["r_verify"], 3),
+                              "repairs": r8[n][1]["repairs"],
+                              "protected_row_equals_reference_prefix":
+                                  r8[n][0][0][:min(len(r8[n][0][0]), len(r8["always_on"][0][0]))] ==
+                                  r8["always_on"][0][0][:min(len(r8[n][0][0]), len(r8["always_on"][0][0]))]}
+                          for n in ("margingate_pipelined", "always_on_pipelined")},
             "note": "rank 0's numbers (times not reduced over ranks)"}
         wseq, wtok, wms, wst = paper["window"]
         t_tok_bf16 = tm["bf16"] / (pb * K)
@@ -510,7 +566,7 @@ def run_reference(args):
             "e2e": {"value": round(v, 5), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
-def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False, flips=None):
+def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False, flips=None, pipelined=False):
     """Fresh prefill of `prompts`, W + K decode steps at threshold tau; eps (a
     list) collects eps_pert per (row, step) -- only valid at tau = inf with
     every row protected, where the verifier's rank k is row k.  flips (a
@@ -528,9 +584,11 @@ def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False, flips=None
             eng.release(i)
         except Exception:
             pass
+    eng.set_policy(verify_mode=1 if pipelined else 0)
     seqs = [[eng.prefill(i, p)] for i, p in enumerate(prompts)]
     s0 = eng.stats()
     capf = capv = None
+    replaced = 0
     if eps is not None:
         capf = torch.empty((B, V), dtype=torch.float32, device="cuda")
         capv = torch.empty((B, V), dtype=torch.float32, device="cuda")
@@ -544,8 +602,13 @@ def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False, flips=None
             e0.record(eng.stream)
         eng.step(rows, prot, tau, out, kind)
         o = out.cpu().numpy()
+        kk = kind.cpu().numpy() if pipelined else None
         for b in range(B):
-            seqs[b].append(int(o[b]))
+            if pipelined and kk[b] == 4:   # MG_VERIFY_PIPELINED: replaces the last (tentative) token
+                seqs[b][-1] = int(o[b])
+                replaced += k >= W
+            else:
+                seqs[b].append(int(o[b]))
         if flips is not None:
             r = eng.last_step(B)
             flips.extend((float(r["g"][b]), bool(r["f_tok"][b] != r["v_tok"][b])) for b in range(B) if r["trig"][b])
@@ -560,8 +623,16 @@ def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False, flips=None
     if eps is not None:
         eng.capture_logits(None)
         eng.capture_verifier_logits(None)
+    if pipelined:
+        pos, last, _ = eng.verify_window(rows)
+        for b in range(B):
+            n = int(pos[b]) - len(prompts[b]) + 1
+            del seqs[b][n:]
+            seqs[b][-1] = int(last[b])
+        eng.set_policy(verify_mode=0)
     s1 = eng.stats()
     st = {k: s1[k] - s0[k] for k in ("protected_rows", "triggers", "repairs")}
+    st["tokens"] = B * K - replaced
     return seqs, st, ms
 
 

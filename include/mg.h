@@ -95,6 +95,24 @@ typedef enum { MG_FAST_BATCH_SHAPED = 0, MG_FAST_BATCH_INVARIANT = 1 } mg_fast_s
  *   MG_REPAIR_TOKEN_ONLY  emit the verifier token, keep the tentative BF16
  *                         column: the ablation of PAPER.md:317. */
 typedef enum { MG_REPAIR_COLUMN = 0, MG_REPAIR_TOKEN_ONLY = 1 } mg_repair_action;
+/* When the verifier runs (mg_set_policy).
+ *   MG_VERIFY_SYNC       the gated rows of a step are verified inside the same
+ *                        mg_decode_step, before it commits;
+ *                        every row's token is final when emitted; default.
+ *   MG_VERIFY_PIPELINED  a gated row's token is emitted TENTATIVELY (kind 3)
+ *                        and verified in the slot's next step, whose forward
+ *                        carries the verifier's catch-up tokens as extra GEMM
+ *                        columns of the same weight pass (the native-runtime
+ *                        lever of PAPER.md:393; SURVEY 7 "hard parts").  If the
+ *                        verifier disagrees, that next step emits kind 4: the
+ *                        verifier token REPLACES the slot's last emitted token,
+ *                        its K/V column is repaired and the slot
+ *                        does not advance.  The committed sequences equal the
+ *                        MG_VERIFY_SYNC ones (the fast path of a row does not
+ *                        depend on the other rows).  A slot with a pending token
+ *                        must be in the next batch (else MG_ERR_STATE) or be
+ *                        resolved with mg_verify_window. */
+typedef enum { MG_VERIFY_SYNC = 0, MG_VERIFY_PIPELINED = 1 } mg_verify_mode;
 
 /* Sizes the four buffers for `cfg`.  MG_ERR_INVALID on unsupported shapes
  * (d_model % 64, d_ff % 64, (H+2KV)*hd % 128, vocab % 128, head_dim in
@@ -122,7 +140,10 @@ mg_status mg_prefill(mg_ctx* ctx, int32_t slot, const int32_t* prompt_host, int3
  *   threshold              tau >= 0; 0 = pure BF16 (r_verify = 0), +INFINITY =
  *                          always-on verification (r_verify = 1)
  *   tokens_out_dev[b]      committed token (int32)
- *   kind_out_dev[b]        nullable: 0 fast, 1 verified, 2 repair
+ *   kind_out_dev[b]        nullable: 0 fast, 1 verified, 2 repair; MG_VERIFY_PIPELINED:
+ *                          0 final, 1 final (the previous tentative token was
+ *                          verified), 3 tentative, 4 the token REPLACES the
+ *                          slot's previous (tentative) token, no new token
  *   margin_out_dev[b]      nullable: fp32 margin g of the fast logits
  * Each row consumes its last committed token at position p and commits exactly
  * one token.  MG_ERR_INVALID: batch not in [1, max_batch], inactive or
@@ -131,10 +152,11 @@ mg_status mg_prefill(mg_ctx* ctx, int32_t slot, const int32_t* prompt_host, int3
 mg_status mg_decode_step(mg_ctx* ctx, const int32_t* slots_host, int32_t batch, const uint8_t* protected_host,
                          float threshold, int32_t* tokens_out_dev, uint8_t* kind_out_dev, float* margin_out_dev);
 
-/* Selects the fast-path schedule and the repair action for later steps
- * (values of mg_fast_schedule / mg_repair_action).  MG_ERR_INVALID for
- * unknown values (no state change). */
-mg_status mg_set_policy(mg_ctx* ctx, int32_t fast_schedule, int32_t repair_action);
+/* Selects the fast-path schedule, the repair action and the verify mode for
+ * later steps (values of mg_fast_schedule / mg_repair_action /
+ * mg_verify_mode).  MG_ERR_INVALID for unknown values, MG_ERR_STATE when the
+ * verify mode changes while tentative tokens are pending (no state change). */
+mg_status mg_set_policy(mg_ctx* ctx, int32_t fast_schedule, int32_t repair_action, int32_t verify_mode);
 
 /* LLM-42-style windowed verification with rollback ("keeps the
  * default path but verifies every token", "verifier setting

@@ -69,7 +69,7 @@ _SIGS = {
     "mg_prefill": [_vp, _i32, _P(_i32), _i32, _P(_i32)],
     "mg_decode_step": [_vp, _P(_i32), _i32, _P(C.c_uint8), _f32, _vp, _vp, _vp],
     "mg_stats": [_vp, _P(MgStats)],
-    "mg_set_policy": [_vp, _i32, _i32],
+    "mg_set_policy": [_vp, _i32, _i32, _i32],
     "mg_verify_window": [_vp, _vp, _i32, _vp, _vp, _vp],
     "mg_release": [_vp, _i32],
     "mg_destroy": [_vp],

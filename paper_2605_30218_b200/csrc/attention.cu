@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
       mbar_expect_tx(&bars[0], C::BLK);
 #pragma unroll
       for (int h = 0; h < C::HALVES; ++h)
-        tma_load_3d(sm + C::Q_OFF + h * 2048, &a.qmap, &bars[0], 64 * h, kvh * G, t);
+        tma_load_3d(sm + C::Q_OFF + h * 2048, &a.qmap, &bars[0], 64 * h, kvh * G, t + a.q_row0);
     }
   } else {
     // QKV epilogue (the same arithmetic as k_epi_qkv): q rows of
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
     // kvn and appended to the cache at position p = n - 1
     constexpr int h2 = HD / 2;
     const int NQKV = (H + 2 * a.KV) * HD;
-    const size_t stride = (size_t)a.T * NQKV, row = (size_t)t * NQKV;
+    const size_t stride = (size_t)(a.part_T ? a.part_T : a.T) * NQKV, row = (size_t)t * NQKV;
     const int p = a.pos[t];
     const int nq = G * h2, nitems = nq + (has_new ? 2 * h2 : 0);
     for (int w = threadIdx.x; w < nitems; w += kAtThreads) {

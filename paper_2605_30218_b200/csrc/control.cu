@@ -132,8 +132,13 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
     slot = a.slots[b];
     p = a.pos[slot];
     s0 = a.shadow_len[slot];
-    const bool prot = a.prot ? a.prot[b] != 0 : true;
-    tr = prot && (a.g[b] < a.tau);  // strict <
+    if (a.pend) {  // pipelined verification: the tentative token sits at position p (= pos - 1 here)
+      tr = a.pend[slot] != 0;
+      p -= 1;
+    } else {
+      const bool prot = a.prot ? a.prot[b] != 0 : true;
+      tr = prot && (a.g[b] < a.tau);  // strict <
+    }
   }
   const int gap = tr ? (p - s0 + 1) : 0;
   // exclusive scans of trig flags and gaps (ascending row order)
@@ -164,6 +169,7 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
   const int r = wsum[warp] + rank_in_warp;
   const int off = wgap[warp] + g_incl - gap;
   a.rank[b] = r;
+  if (a.rank_slot) a.rank_slot[slot] = r;
   a.ctrl[2 + r] = b;
   a.last[r] = off + gap - 1;
   const int32_t* h = a.hist + (size_t)slot * a.hist_stride;
@@ -327,6 +333,7 @@ __global__ void k_window_commit(WindowArgs a) {
     a.pos[slot] = np;
   }
   a.shadow_len[slot] = np;
+  if (a.pend) a.pend[slot] = 0;
   a.res[3 * i] = np;
   a.res[3 * i + 1] = h[np];
   a.res[3 * i + 2] = rb;
@@ -341,6 +348,127 @@ __global__ void k_window_commit(WindowArgs a) {
 
 cudaError_t launch_window_commit(const WindowArgs& a, cudaStream_t st) {
   return launch_k(k_window_commit, dim3(a.n), dim3(32), 0, st, a);
+}
+
+// ------------------------------------------------------------------ pipelined verification
+// (include/mg.h MG_VERIFY_PIPELINED).  The rows gated at step t are verified
+// inside step t+1's forward (their catch-up tokens are extra GEMM columns --
+// the tcgen05 GEMM's per-column result is independent of the other columns,
+// and a separate pinned-split attention launch over the
+// shadow cache).  Row b of step t+1, slot s, tentative token y at position p:
+//   pending and v == y: verified (shadow_len = p); the step's fast output stands
+//   pending and v != y: repair -- hist[p] = v, shadow column p-1 -> fast cache
+//                       (PAPER.md:208), the row does not advance (its fast
+//                       output was computed from y and is dropped), kind 4
+//   then (not repaired): commit f_tok at p+1; gated = prot && g < tau ->
+//                        pending (kind 3), else kind 0 (1 if a pending token
+//                        was just verified)
+__global__ void __launch_bounds__(256) k_commit_fused(FusedCommitArgs a) {
+  griddep();
+  const int b = blockIdx.x;
+  const int slot = a.slots[b];
+  const int p = a.pos[slot];
+  int32_t* h = a.hist + (size_t)slot * a.hist_stride;
+  const bool pend = a.had_pend && a.pend[slot];
+  const int v = pend ? a.v_tok[a.rank_slot[slot]] : -1;
+  const bool rep = pend && v != h[p];
+  if (rep && a.repair_copy) copy_cols(a.copy, slot, p - 1, p, threadIdx.x, blockDim.x);
+  if (threadIdx.x != 0) return;
+  const bool prot = a.prot ? a.prot[b] != 0 : true;
+  unsigned long long* s = a.stats;
+  atomicAdd(&s[1], 1ull);
+  if (prot) atomicAdd(&s[2], 1ull);
+  if (pend) atomicAdd(&s[rep ? 5 : 4], 1ull);
+  if (b == 0) {
+    atomicAdd(&s[0], 1ull);
+    if (a.had_pend && a.n_pend > 0) {
+      atomicAdd(&s[6], 1ull);
+      atomicAdd(&s[7], (unsigned long long)a.M);
+    }
+  }
+  int kind, out;
+  bool gated = false;
+  if (pend) a.shadow_len[slot] = p;  // shadow columns 0..p-1 are final
+  if (rep) {
+    h[p] = v;
+    a.pend[slot] = 0;
+    kind = 4;
+    out = v;
+  } else {
+    out = a.f_tok[b];
+    gated = a.gate_on && prot && a.g[b] < a.tau;  // strict <
+    h[p + 1] = out;
+    a.pos[slot] = p + 1;
+    a.pend[slot] = gated ? 1 : 0;
+    kind = gated ? 3 : (pend ? 1 : 0);
+    if (gated) atomicAdd(&s[3], 1ull);
+  }
+  a.tokens_out[b] = out;
+  if (a.kind_out) a.kind_out[b] = (uint8_t)kind;
+  if (a.margin_out) a.margin_out[b] = a.g[b];
+  if (a.dbg_vtok) {
+    a.dbg_vtok[b] = v;
+    a.dbg_vg[b] = pend ? a.v_g[a.rank_slot[slot]] : 0.f;
+    a.dbg_kind[b] = (uint8_t)kind;
+    a.dbg_trig[b] = gated ? 1 : 0;
+    a.dbg_out[b] = out;
+  }
+}
+
+cudaError_t launch_commit_fused(const FusedCommitArgs& a, cudaStream_t st) {
+  return launch_k(k_commit_fused, dim3(a.B), dim3(256), 0, st, a);
+}
+
+// M = the bucketed catch-up length of the launch; the real one is ctrl[1]
+// (written by the pending-list gate of the previous step).  Padding rows
+// repeat the last real entry: they recompute the same shadow column from the
+// same inputs (identical values), so the padding changes nothing but keeps
+// the number of distinct CUDA graphs small.
+__global__ void k_prepare_mixed(const int32_t* __restrict__ slots, int B, const int32_t* __restrict__ pos,
+                                const int32_t* __restrict__ hist, int hist_stride, const int32_t* cu_slot,
+                                const int32_t* cu_pos, const int32_t* cu_tok, const int32_t* cu_nk, int M,
+                                const int32_t* __restrict__ ctrl, int32_t* m_slot, int32_t* m_pos, int32_t* m_tok,
+                                int32_t* m_nk) {
+  griddep();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < B) {
+    const int s = slots[i], p = pos[s];
+    m_slot[i] = s;
+    m_pos[i] = p;
+    m_tok[i] = hist[(size_t)s * hist_stride + p];
+    m_nk[i] = p + 1;
+  } else if (i < B + M) {
+    const int e = min(i - B, ctrl[1] - 1);
+    m_slot[i] = cu_slot[e];
+    m_pos[i] = cu_pos[e];
+    m_tok[i] = cu_tok[e];
+    m_nk[i] = cu_nk[e];
+  }
+}
+
+cudaError_t launch_prepare_mixed(const int32_t* slots, int B, const int32_t* pos, const int32_t* hist, int hist_stride,
+                                 const int32_t* cu_slot, const int32_t* cu_pos, const int32_t* cu_tok,
+                                 const int32_t* cu_nk, int M, const int32_t* ctrl, int32_t* m_slot, int32_t* m_pos,
+                                 int32_t* m_tok, int32_t* m_nk, cudaStream_t st) {
+  return launch_k(k_prepare_mixed, dim3((B + M + 127) / 128), dim3(128), 0, st, slots, B, pos, hist, hist_stride,
+                  cu_slot, cu_pos, cu_tok, cu_nk, M, ctrl, m_slot, m_pos, m_tok, m_nk);
+}
+
+// one CTA per output row, 16-byte copies; verifier rows past the real count
+// ctrl[0] (bucket padding) repeat the last real one
+__global__ void k_lm_rows(const uint16_t* __restrict__ src, int B, const int32_t* __restrict__ last,
+                          const int32_t* __restrict__ ctrl, int d, uint16_t* __restrict__ dst) {
+  griddep();
+  const int i = blockIdx.x;
+  const int r = i < B ? i : B + last[min(i - B, ctrl[0] - 1)];
+  const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)r * d);
+  uint4* o = reinterpret_cast<uint4*>(dst + (size_t)i * d);
+  for (int j = threadIdx.x; j < d / 8; j += blockDim.x) o[j] = s[j];
+}
+
+cudaError_t launch_lm_rows(const uint16_t* src, int B, const int32_t* last, const int32_t* ctrl, int n, int d,
+                           uint16_t* dst, cudaStream_t st) {
+  return launch_k(k_lm_rows, dim3(B + n), dim3(128), 0, st, src, B, last, ctrl, d, dst);
 }
 
 // prefill bookkeeping: hist[slot][len] = token, pos = shadow_len = len

@@ -23,6 +23,11 @@ struct GateArgs {
   int32_t* cu_pos;
   int32_t* cu_tok;
   int32_t* cu_nk;
+  // pipelined verification (MG_VERIFY_PIPELINED): when pend != nullptr the
+  // rows to verify are the slots with pend[slot] = 1 (their tentative token
+  // sits at position pos - 1) instead of prot && g < tau
+  const uint8_t* pend;     // [max_slots] or nullptr
+  int32_t* rank_slot;      // [max_slots] rank of each listed slot (nullable)
 };
 cudaError_t launch_gate(const GateArgs& a, cudaStream_t st);
 
@@ -81,9 +86,52 @@ struct WindowArgs {
   const int32_t* v_tok;    // [M] verifier argmax of every catch-up token
   int32_t* res;            // [3n]: new pos, last token, rolled-back count
   unsigned long long* stats;
+  uint8_t* pend;           // [max_slots] pipelined-verification flags, cleared (nullable)
 };
 cudaError_t launch_window_list(const WindowArgs& a, cudaStream_t st);
 cudaError_t launch_window_commit(const WindowArgs& a, cudaStream_t st);
+
+// pipelined verification: commit of one step (include/mg.h, MG_VERIFY_PIPELINED)
+struct FusedCommitArgs {
+  int B;
+  const int32_t* slots;
+  const uint8_t* prot;     // [B] or nullptr
+  float tau;
+  int gate_on;             // any protected row && tau > 0
+  int had_pend;            // this step verified the pending slots (v_tok valid)
+  uint8_t* pend;           // [max_slots]
+  const int32_t* rank_slot;
+  const int32_t* f_tok;
+  const float* g;
+  const int32_t* v_tok;    // [n_pend] by rank
+  const float* v_g;
+  int32_t* pos;
+  int32_t* shadow_len;
+  int32_t* hist;
+  int hist_stride;
+  ColCopy copy;            // shadow -> fast
+  int repair_copy;
+  int32_t* tokens_out;
+  uint8_t* kind_out;
+  float* margin_out;
+  unsigned long long* stats;
+  int32_t n_pend, M;       // verifier accounting of this step
+  int32_t* dbg_vtok;
+  float* dbg_vg;
+  uint8_t* dbg_kind;
+  uint8_t* dbg_trig;
+  int32_t* dbg_out;
+};
+cudaError_t launch_commit_fused(const FusedCommitArgs& a, cudaStream_t st);
+// mixed token list: rows [0,B) the fast rows (slot, pos, hist[pos], pos+1),
+// rows [B, B+M) a copy of the catch-up list cu_*[0, M)
+cudaError_t launch_prepare_mixed(const int32_t* slots, int B, const int32_t* pos, const int32_t* hist, int hist_stride,
+                                 const int32_t* cu_slot, const int32_t* cu_pos, const int32_t* cu_tok,
+                                 const int32_t* cu_nk, int M, const int32_t* ctrl /* [1] = real M */,
+                                 int32_t* m_slot, int32_t* m_pos, int32_t* m_tok, int32_t* m_nk, cudaStream_t st);
+// LM-head input rows: dst[i] = src[i] for i < B, dst[B + r] = src[B + last[min(r, ctrl[0]-1)]] for r < n
+cudaError_t launch_lm_rows(const uint16_t* src, int B, const int32_t* last, const int32_t* ctrl, int n, int d,
+                           uint16_t* dst, cudaStream_t st);
 
 cudaError_t launch_prepare(const int32_t* slots, int B, const int32_t* pos, const int32_t* hist, int hist_stride,
                            int32_t* f_slot, int32_t* f_pos, int32_t* f_tok, int32_t* f_nk, cudaStream_t st);

@@ -181,8 +181,9 @@ __global__ void k_epi_qkv(const float* __restrict__ part, PartSpec ps, QkvArgs a
 cudaError_t launch_epi_qkv(const float* part, PartSpec ps, const uint16_t* bias, const int32_t* pos, int T, int H,
                            int KV, int hd, const float* rope_cos, const float* rope_sin, uint16_t* q,
                            const CacheView* cache, const int32_t* slot, uint16_t* k_out, uint16_t* v_out,
-                           cudaStream_t st) {
+                           cudaStream_t st, int part_T) {
   QkvArgs a{};
+  a.part_T = part_T;
   a.bias = bias; a.pos = pos; a.T = T; a.H = H; a.KV = KV; a.hd = hd; a.rcos = rope_cos; a.rsin = rope_sin;
   a.q = q; a.paged = cache != nullptr; a.slot = slot; a.kd = k_out; a.vd = v_out;
   if (cache) a.cache = *cache;

@@ -273,12 +273,13 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   c->xg = s.take<uint16_t>((size_t)B * c->d);
   c->xgn = s.take<uint16_t>((size_t)B * c->d);
   c->part = s.take<float>(c->part_elems);
-  c->logits = s.take<float>((size_t)Tm * c->V);  // window verify: LM head over whole chunks
+  const size_t Tlm = (size_t)(Tm > 2 * B ? Tm : 2 * B);
+  c->logits = s.take<float>(Tlm * c->V);  // window verify: LM head over whole chunks; pipelined: 2B rows
   c->attn_acc = s.take<float>(attn_rows * c->hd);
   c->attn_ml = s.take<float>(attn_rows * 2);
   c->attn_cnt = s.take<int32_t>((size_t)Tm * c->KV);
   c->chain_sync = s.take<uint32_t>(2 * kChainMax + 1);
-  c->top2_part = s.take<float>((size_t)Tm * c->nb_top2 * 4);
+  c->top2_part = s.take<float>(Tlm * c->nb_top2 * 4);
   c->rope_cos = s.take<float>((size_t)g.max_seq * (c->hd / 2));
   c->rope_sin = s.take<float>((size_t)g.max_seq * (c->hd / 2));
   c->pos_d = s.take<int32_t>(g.max_slots);
@@ -302,6 +303,11 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   c->v_tok = s.take<int32_t>(B); c->v_i2 = s.take<int32_t>(B);
   c->v_g = s.take<float>(B); c->v_v1 = s.take<float>(B); c->v_v2 = s.take<float>(B);
   c->w_tok = s.take<int32_t>(cu);
+  c->pend_d = s.take<uint8_t>(g.max_slots);
+  c->rank_slot_d = s.take<int32_t>(g.max_slots);
+  c->mx_slot = s.take<int32_t>(Tm); c->mx_pos = s.take<int32_t>(Tm);
+  c->mx_tok = s.take<int32_t>(Tm); c->mx_nk = s.take<int32_t>(Tm);
+  c->xlm = s.take<uint16_t>((size_t)2 * B * c->d);
   c->w_res = s.take<int32_t>(3 * (size_t)B);
   {
     const size_t a4 = 4 * (size_t)B, b2 = 2 * (size_t)c->max_pages;
@@ -434,6 +440,63 @@ static mg_status forward(mg_ctx* c, int T, const int32_t* slot, const int32_t* p
     const uint16_t* wn = l + 1 < c->L ? c->layers[l + 1].attn_norm : c->final_norm;
     CK(launch_residual_norm(c->x, c->part, sc.down.ps(), T, c->d, wn, eps, c->xn, c->st));
     c->launches += fuse ? 4 : 5;
+  }
+  return MG_OK;
+}
+
+// Pipelined verification (MG_VERIFY_PIPELINED): B fast rows (mx rows [0,B),
+// fast cache, schedule fs) and M verifier catch-up tokens (mx rows [B, B+M),
+// shadow cache, pinned schedule ds) in ONE pass over the weights: every GEMM
+// runs on the B+M columns (a column's result does not depend on the others,
+// DESIGN.md 7.2), attention is launched once per row group with its own cache
+// and split schedule.
+static mg_status forward_mixed(mg_ctx* c, int B, int M, const Sched& fs, const Sched& ds) {
+  const int T = B + M, Tm = c->Tmax;
+  const float eps = c->cfg.rms_eps;
+  const OpSched oq = op_det(c->NQKV, c->d, T), oo = op_det(c->d, c->NQ, T), ogu = op_det(2 * c->F, c->d, T),
+                od = op_det(c->d, c->F, T);
+  CK(launch_embed(c->embed, c->mx_tok, T, c->d, c->x, c->st));
+  CK(launch_rmsnorm(c->x, c->layers[0].attn_norm, T, c->d, eps, c->xn, c->st));
+  c->launches += 2;
+  for (int l = 0; l < c->L; ++l) {
+    const LayerW& w = c->layers[l];
+    mg_status r = gemm(c, c->xn, Tm, T, w.qkv, oq, c->part);
+    if (r) return r;
+    // fast rows: QKV epilogue fused into attention, fast cache, batch-shaped splits
+    CacheView cf = cache_view(c, 0, l);
+    AttnArgs aa{};
+    aa.q = c->q; aa.cache = cf; aa.paged = 1; aa.slot = c->mx_slot; aa.n_keys = c->mx_nk;
+    aa.T = B; aa.H = c->H; aa.KV = c->KV; aa.hd = c->hd; aa.split_keys = fs.attn_sk; aa.n_splits = fs.attn_ns;
+    aa.part_acc = c->attn_acc; aa.part_ml = c->attn_ml; aa.out = c->att;
+    aa.qmap = c->attn_qmap; aa.kmap = aa.vmap = c->kv_map[0]; aa.counter = c->attn_cnt;
+    aa.prewait = 1; aa.fuse_qkv = 1;
+    aa.qkv_part = c->part; aa.qkv_ps = oq.ps(); aa.bias = w.bqkv; aa.pos = c->mx_pos;
+    aa.rcos = c->rope_cos; aa.rsin = c->rope_sin; aa.part_T = T;
+    CK(launch_attention(aa, c->st));
+    c->launches++;
+    if (M > 0) {
+      // verifier rows: separate epilogue into the shadow cache, pinned splits
+      CacheView cs = cache_view(c, 1, l);
+      CK(launch_epi_qkv(c->part + (size_t)B * c->NQKV, oq.ps(), w.bqkv, c->mx_pos + B, M, c->H, c->KV, c->hd,
+                        c->rope_cos, c->rope_sin, c->q + (size_t)B * c->NQ, &cs, c->mx_slot + B, nullptr, nullptr,
+                        c->st, T));
+      AttnArgs av{};
+      av.q = c->q; av.cache = cs; av.paged = 1; av.slot = c->mx_slot + B; av.n_keys = c->mx_nk + B;
+      av.T = M; av.H = c->H; av.KV = c->KV; av.hd = c->hd; av.split_keys = ds.attn_sk; av.n_splits = ds.attn_ns;
+      av.part_acc = c->attn_acc; av.part_ml = c->attn_ml; av.out = c->att + (size_t)B * c->NQ;
+      av.qmap = c->attn_qmap; av.kmap = av.vmap = c->kv_map[1]; av.counter = c->attn_cnt;
+      av.q_row0 = B;
+      CK(launch_attention(av, c->st));
+      c->launches += 2;
+    }
+    if ((r = gemm(c, c->att, Tm, T, w.o, oo, c->part))) return r;
+    CK(launch_residual_norm(c->x, c->part, oo.ps(), T, c->d, w.mlp_norm, eps, c->xn, c->st));
+    if ((r = gemm(c, c->xn, Tm, T, w.gu, ogu, c->part))) return r;
+    CK(launch_epi_swiglu(c->part, ogu.ps(), T, c->F, c->a, c->st));
+    if ((r = gemm(c, c->a, Tm, T, w.down, od, c->part))) return r;
+    const uint16_t* wn = l + 1 < c->L ? c->layers[l + 1].attn_norm : c->final_norm;
+    CK(launch_residual_norm(c->x, c->part, od.ps(), T, c->d, wn, eps, c->xn, c->st));
+    c->launches += 3;
   }
   return MG_OK;
 }
@@ -718,6 +781,182 @@ static mg_status gen_weights(mg_ctx* c) {
 }
 
 // ================================================================== C ABI
+// ---- pipelined verification (MG_VERIFY_PIPELINED) ---------------------
+// Readback of a pipelined step (pinned, one copy each):
+//   [ctrl: 2 + B] [last: B] [pos: S] [shadow_len: S] [pend: S bytes]
+static size_t fpin_words(const mg_ctx* c) {
+  const size_t B = c->cfg.max_batch, S = c->cfg.max_slots;
+  return 2 + 2 * B + 2 * S + (S + 3) / 4 + 4;
+}
+
+// Wait for the previous pipelined step and refresh the host mirrors from it.
+static mg_status pipe_refresh(mg_ctx* c) {
+  if (!c->f_sync) return MG_OK;
+  CK(cudaEventSynchronize(c->fev));
+  c->f_sync = false;
+  const int B = c->cfg.max_batch, S = c->cfg.max_slots;
+  const int32_t* pos = c->fpin + 2 + 2 * B;
+  const int32_t* sh = pos + S;
+  const uint8_t* pe = reinterpret_cast<const uint8_t*>(sh + S);
+  for (int i = 0; i < S; ++i) {
+    if (!c->active[i]) continue;
+    c->pos_h[i] = pos[i];
+    c->shadow_h[i] = sh[i];
+    c->pend_h[i] = pe[i];
+  }
+  return MG_OK;
+}
+
+static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const uint8_t* prot, float tau,
+                                  int32_t* tokens_out, uint8_t* kind_out, float* margin_out) {
+  mg_status r = pipe_refresh(c);
+  if (r) return r;
+  const int S = c->cfg.max_slots;
+  std::vector<char> seen(S, 0);
+  int max_ctx = 1, need_pages = 0;
+  bool any_prot = false;
+  for (int b = 0; b < B; ++b) {
+    const int s = slots[b];
+    if (s < 0 || s >= S || !c->active[s] || seen[s]) return fail(c, MG_ERR_INVALID, "inactive or duplicate slot");
+    seen[s] = 1;
+    const int p = c->pos_h[s];
+    if (p >= c->cfg.max_seq) return fail(c, MG_ERR_CAPACITY, "max_seq reached");
+    if (p / c->PS >= (int)c->pages[s].size()) ++need_pages;
+    if (p + 1 > max_ctx) max_ctx = p + 1;
+    if (!prot || prot[b]) any_prot = true;
+  }
+  for (int s = 0; s < S; ++s)
+    if (c->active[s] && c->pend_h[s] && !seen[s])
+      return fail(c, MG_ERR_STATE, "a slot with a pending tentative token is missing from the batch "
+                                   "(include it or call mg_verify_window)");
+  if ((int)c->free_pages.size() < need_pages) return fail(c, MG_ERR_CAPACITY, "KV pages exhausted");
+  // the pending list built at the end of the previous step (device ctrl / last / cu_*)
+  const int32_t* ctrl_h = c->fpin;
+  int n_pend = 0, M = 0, vmax = 1;
+  std::vector<int> last;
+  for (int s = 0; s < S; ++s) n_pend += c->active[s] && c->pend_h[s];
+  if (n_pend > 0) {
+    if (ctrl_h[0] != n_pend) return fail(c, MG_ERR_CUDA, "pending list mismatch between host mirror and device");
+    M = ctrl_h[1];
+    last.assign(ctrl_h + 2 + c->cfg.max_batch, ctrl_h + 2 + c->cfg.max_batch + n_pend);
+    for (int s = 0; s < S; ++s)
+      if (c->active[s] && c->pend_h[s] && c->pos_h[s] > vmax) vmax = c->pos_h[s];
+  }
+  size_t ev0 = 0;
+  if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
+  // upload batch + protection mask + page-table updates (as mg_decode_step)
+  std::vector<std::pair<int, int>> upd;
+  for (int b = 0; b < B; ++b) {
+    const int s = slots[b];
+    if (c->pos_h[s] / c->PS >= (int)c->pages[s].size()) alloc_page(c, s, &upd);
+  }
+  {
+    const int pw = (B + 3) / 4;
+    std::vector<int32_t> w(B + pw + 2 * upd.size());
+    memcpy(w.data(), slots, B * 4);
+    std::vector<uint8_t> pb(pw * 4, 1);
+    if (prot) memcpy(pb.data(), prot, B);
+    memcpy(w.data() + B, pb.data(), pw * 4);
+    for (size_t i = 0; i < upd.size(); ++i) {
+      w[B + pw + 2 * i] = upd[i].first;
+      w[B + pw + 2 * i + 1] = upd[i].second;
+    }
+    if ((r = upload(c, w))) return r;
+    CK(cudaMemcpyAsync(c->slots_d, c->staging_d, B * 4, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(c->prot_d, c->staging_d + B, B, cudaMemcpyDeviceToDevice, c->st));
+    if (!upd.empty()) {
+      k_apply_pt<<<cdiv((int)upd.size(), 128), 128, 0, c->st>>>(c->pt_d, c->staging_d + B + pw, (int)upd.size());
+      CK(cudaGetLastError());
+      c->launches++;
+    }
+  }
+  // catch-up too long to ride along: the pending rows' verifier runs on its own first
+  int Mx = M;
+  if (M > 0 && B + M > c->Tmax) {
+    CK(cudaMemcpyAsync(c->last_d, last.data(), n_pend * 4, cudaMemcpyHostToDevice, c->st));
+    if ((r = run_det(c, M, last, vmax))) return r;
+    Mx = 0;
+  }
+  // bucket the catch-up length and the verifier LM rows to powers of two (padding
+  // repeats real entries, k_prepare_mixed / k_lm_rows): few distinct graphs
+  int Mb = Mx, n_lm = Mx > 0 ? n_pend : 0;
+  if (Mx > 0) {
+    Mb = 1;
+    while (Mb < Mx) Mb <<= 1;
+    if (B + Mb > c->Tmax) Mb = Mx;
+    int nb = 1;
+    while (nb < n_lm) nb <<= 1;
+    n_lm = nb < B ? nb : B;
+  }
+  Mx = Mb;
+  Sched fs = sched_fast(c, B, max_ctx);
+  Sched ds = sched_det(c, Mx > 0 ? Mx : 1, vmax);
+  r = graphed(c, std::make_tuple(3, B, Mx, n_lm, fs.attn_ns * 65536 + ds.attn_ns, fs.attn_sk), [&]() -> mg_status {
+    CK(launch_prepare_mixed(c->slots_d, B, c->pos_d, c->hist_d, c->cfg.max_seq + 1, c->cu_slot, c->cu_pos, c->cu_tok,
+                            c->cu_nk, Mx, c->ctrl_d, c->mx_slot, c->mx_pos, c->mx_tok, c->mx_nk, c->st));
+    c->launches++;
+    mg_status rr = forward_mixed(c, B, Mx, fs, ds);
+    if (rr) return rr;
+    CK(launch_lm_rows(c->xn, B, c->last_d, c->ctrl_d, n_lm, c->d, c->xlm, c->st));
+    c->launches++;
+    const int T = B + n_lm;
+    if ((rr = gemm(c, c->xlm, 2 * c->cfg.max_batch, T, c->lm, op_lm(c->V, c->d, T, true), c->logits))) return rr;
+    CK(launch_top2(c->logits, B, c->V, c->top2_part, c->nb_top2, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g,
+                   c->nan_d, c->st));
+    c->launches += 2;
+    if (n_lm > 0) {
+      CK(launch_top2(c->logits + (size_t)B * c->V, n_lm, c->V, c->top2_part + (size_t)B * c->nb_top2 * 4,
+                     c->nb_top2, c->v_v1, c->v_tok, c->v_v2, c->v_i2, c->v_g, c->nan_d, c->st));
+      c->launches += 2;
+    }
+    return MG_OK;
+  });
+  if (r) return r;
+  if (c->capture) CK(cudaMemcpyAsync(c->capture, c->logits, (size_t)B * c->V * 4, cudaMemcpyDeviceToDevice, c->st));
+  if (c->capture_v && n_lm > 0)
+    CK(cudaMemcpyAsync(c->capture_v, c->logits + (size_t)B * c->V, (size_t)n_lm * c->V * 4,
+                       cudaMemcpyDeviceToDevice, c->st));
+  // commit + the pending list of the next step
+  FusedCommitArgs fa{};
+  fa.B = B; fa.slots = c->slots_d; fa.prot = c->prot_d; fa.tau = tau; fa.gate_on = any_prot && tau > 0.f;
+  fa.had_pend = n_pend > 0; fa.pend = c->pend_d; fa.rank_slot = c->rank_slot_d;
+  fa.f_tok = c->f_tok; fa.g = c->f_g; fa.v_tok = c->v_tok; fa.v_g = c->v_g;
+  fa.pos = c->pos_d; fa.shadow_len = c->shadow_d; fa.hist = c->hist_d; fa.hist_stride = c->cfg.max_seq + 1;
+  fa.copy = col_copy(c, true); fa.repair_copy = c->repair_mode == MG_REPAIR_COLUMN ? 1 : 0;
+  fa.tokens_out = tokens_out; fa.kind_out = kind_out; fa.margin_out = margin_out; fa.stats = c->stats_d;
+  fa.n_pend = n_pend; fa.M = M;
+  fa.dbg_vtok = c->dbg_vtok; fa.dbg_vg = c->dbg_vg; fa.dbg_kind = c->dbg_kind; fa.dbg_trig = c->dbg_trig;
+  fa.dbg_out = c->dbg_out;
+  CK(launch_commit_fused(fa, c->st));
+  GateArgs ga{};
+  ga.g = c->f_g; ga.prot = c->prot_d; ga.tau = tau; ga.slots = c->slots_d; ga.B = B;
+  ga.pos = c->pos_d; ga.shadow_len = c->shadow_d; ga.hist = c->hist_d; ga.hist_stride = c->cfg.max_seq + 1;
+  ga.trig = c->trig_d; ga.rank = c->rank_d; ga.ctrl = c->ctrl_d; ga.last = c->last_d;
+  ga.cu_slot = c->cu_slot; ga.cu_pos = c->cu_pos; ga.cu_tok = c->cu_tok; ga.cu_nk = c->cu_nk;
+  ga.pend = c->pend_d; ga.rank_slot = c->rank_slot_d;
+  CK(launch_gate(ga, c->st));
+  c->launches += 2;
+  // readback for the next step (pending list, mirrors)
+  {
+    const int MB = c->cfg.max_batch;
+    int32_t* f = c->fpin;
+    CK(cudaMemcpyAsync(f, c->ctrl_d, (2 + B) * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(f + 2 + MB, c->last_d, B * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(f + 2 + 2 * MB, c->pos_d, S * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(f + 2 + 2 * MB + S, c->shadow_d, S * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(f + 2 + 2 * MB + 2 * S, c->pend_d, S, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaEventRecord(c->fev, c->st));
+    c->f_sync = true;
+  }
+  if (c->timing.on) {
+    cudaEventRecord(tevent(c), c->st);
+    c->timing.rec.emplace_back(ev0, c->timing.used - 1, 2, 0.0);
+  }
+  for (int b = 0; b < B; ++b) c->pos_h[slots[b]] += 1;  // optimistic; pipe_refresh corrects repairs
+  c->last_B = B;
+  return MG_OK;
+}
+
 static std::string g_init_err;
 
 extern "C" {
@@ -803,6 +1042,10 @@ mg_status mg_init(const mg_config* cfg, const mg_buffers* bufs, void* stream, mg
     const char* f = getenv("MG_CHAIN_PF");  // A/B knob: L2 run-ahead in 16 KB k-blocks
     c->chain_pf = f ? atoi(f) : 0;
   }
+  if ((e = cudaMallocHost(&c->fpin, fpin_words(c) * 4)) || (e = cudaEventCreateWithFlags(&c->fev, cudaEventDisableTiming)))
+    return die(cudaGetErrorString(e));
+  memset(c->fpin, 0, fpin_words(c) * 4);
+  c->pend_h.assign(c->cfg.max_slots, 0);
   c->pos_h.assign(c->cfg.max_slots, 0);
   c->shadow_h.assign(c->cfg.max_slots, 0);
   c->active.assign(c->cfg.max_slots, 0);
@@ -818,6 +1061,7 @@ mg_status mg_prefill(mg_ctx* c, int32_t slot, const int32_t* prompt, int32_t len
   if (slot < 0 || slot >= c->cfg.max_slots || !prompt || len < 1 || !first_token)
     return fail(c, MG_ERR_INVALID, "bad prefill arguments");
   if (c->active[slot]) return fail(c, MG_ERR_STATE, "slot already active");
+  if (pipe_refresh(c)) return MG_ERR_CUDA;
   if (len + 1 > c->cfg.max_seq) return fail(c, MG_ERR_CAPACITY, "prompt longer than max_seq - 1");
   for (int i = 0; i < len; ++i)
     if (prompt[i] < 0 || prompt[i] >= c->V) return fail(c, MG_ERR_INVALID, "token id out of range");
@@ -856,6 +1100,8 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
   if (c->dead) return fail(c, MG_ERR_CUDA, "context is dead: " + c->err);
   if (!slots || !tokens_out || B < 1 || B > c->cfg.max_batch) return fail(c, MG_ERR_INVALID, "bad batch");
   if (std::isnan(tau) || tau < 0.f) return fail(c, MG_ERR_INVALID, "threshold must be >= 0");
+  if (c->verify_mode == MG_VERIFY_PIPELINED)
+    return decode_pipelined(c, slots, B, prot, tau, tokens_out, kind_out, margin_out);
   std::vector<char> seen(c->cfg.max_slots, 0);
   int max_ctx = 1;
   int need_pages = 0;
@@ -975,15 +1221,24 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
   return MG_OK;
 }
 
-mg_status mg_set_policy(mg_ctx* c, int32_t fast_schedule, int32_t repair_action) {
+mg_status mg_set_policy(mg_ctx* c, int32_t fast_schedule, int32_t repair_action, int32_t verify_mode) {
   if (!c) return MG_ERR_INVALID;
   if (c->dead) return fail(c, MG_ERR_CUDA, "context is dead: " + c->err);
   if (fast_schedule != MG_FAST_BATCH_SHAPED && fast_schedule != MG_FAST_BATCH_INVARIANT)
     return fail(c, MG_ERR_INVALID, "unknown fast schedule");
   if (repair_action != MG_REPAIR_COLUMN && repair_action != MG_REPAIR_TOKEN_ONLY)
     return fail(c, MG_ERR_INVALID, "unknown repair action");
+  if (verify_mode != MG_VERIFY_SYNC && verify_mode != MG_VERIFY_PIPELINED)
+    return fail(c, MG_ERR_INVALID, "unknown verify mode");
+  mg_status r = pipe_refresh(c);
+  if (r) return r;
+  if (verify_mode != c->verify_mode)
+    for (int s = 0; s < c->cfg.max_slots; ++s)
+      if (c->active[s] && c->pend_h[s])
+        return fail(c, MG_ERR_STATE, "pending tentative tokens: call mg_verify_window before switching modes");
   c->fast_mode = fast_schedule;
   c->repair_mode = repair_action;
+  c->verify_mode = verify_mode;
   return MG_OK;
 }
 
@@ -993,6 +1248,8 @@ mg_status mg_verify_window(mg_ctx* c, const int32_t* slots, int32_t n, int32_t* 
   if (!c) return MG_ERR_INVALID;
   if (c->dead) return fail(c, MG_ERR_CUDA, "context is dead: " + c->err);
   if (!slots || n < 1 || n > c->cfg.max_batch) return fail(c, MG_ERR_INVALID, "bad window batch");
+  mg_status rf = pipe_refresh(c);
+  if (rf) return rf;
   std::vector<char> seen(c->cfg.max_slots, 0);
   for (int i = 0; i < n; ++i) {
     const int s = slots[i];
@@ -1016,7 +1273,7 @@ mg_status mg_verify_window(mg_ctx* c, const int32_t* slots, int32_t n, int32_t* 
   wa.n = n; wa.slots = c->staging_d; wa.off = c->staging_d + n;
   wa.pos = c->pos_d; wa.shadow_len = c->shadow_d; wa.hist = c->hist_d; wa.hist_stride = c->cfg.max_seq + 1;
   wa.cu_slot = c->cu_slot; wa.cu_pos = c->cu_pos; wa.cu_tok = c->cu_tok; wa.cu_nk = c->cu_nk;
-  wa.v_tok = c->w_tok; wa.res = c->w_res; wa.stats = c->stats_d;
+  wa.v_tok = c->w_tok; wa.res = c->w_res; wa.stats = c->stats_d; wa.pend = c->pend_d;
   if (M > 0) {
     CK(launch_window_list(wa, c->st));
     c->launches++;
@@ -1048,6 +1305,7 @@ mg_status mg_verify_window(mg_ctx* c, const int32_t* slots, int32_t n, int32_t* 
     const int s = slots[i];
     c->pos_h[s] = res[3 * i];
     c->shadow_h[s] = res[3 * i];
+    c->pend_h[s] = 0;
     if (pos_out) pos_out[i] = res[3 * i];
     if (last_out) last_out[i] = res[3 * i + 1];
     if (rb_out) rb_out[i] = res[3 * i + 2];
@@ -1058,6 +1316,8 @@ mg_status mg_verify_window(mg_ctx* c, const int32_t* slots, int32_t n, int32_t* 
 mg_status mg_stats(mg_ctx* c, mg_stats_t* out) {
   if (!c || !out) return MG_ERR_INVALID;
   if (c->dead) return fail(c, MG_ERR_CUDA, "context is dead: " + c->err);
+  mg_status rf = pipe_refresh(c);
+  if (rf) return rf;
   unsigned long long s[16];
   int32_t flags[2] = {0, 0};  // [0] NaN logit, [1] layer-chain grid barrier timed out
   CK(cudaMemcpyAsync(s, c->stats_d, sizeof(s), cudaMemcpyDeviceToHost, c->st));
@@ -1076,6 +1336,12 @@ mg_status mg_release(mg_ctx* c, int32_t slot) {
   if (!c) return MG_ERR_INVALID;
   if (slot < 0 || slot >= c->cfg.max_slots) return fail(c, MG_ERR_INVALID, "bad slot");
   if (!c->active[slot]) return fail(c, MG_ERR_STATE, "slot not active");
+  mg_status rf = pipe_refresh(c);
+  if (rf) return rf;
+  if (c->pend_h[slot]) {
+    CK(cudaMemsetAsync(c->pend_d + slot, 0, 1, c->st));
+    c->pend_h[slot] = 0;
+  }
   for (int p : c->pages[slot]) c->free_pages.push_back(p);
   c->pages[slot].clear();
   c->active[slot] = 0;
@@ -1093,6 +1359,8 @@ void mg_destroy(mg_ctx* c) {
   if (c->stage_ev[0]) cudaEventDestroy(c->stage_ev[0]);
   if (c->stage_ev[1]) cudaEventDestroy(c->stage_ev[1]);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->fpin) cudaFreeHost(c->fpin);
+  if (c->fev) cudaEventDestroy(c->fev);
   if (c->chain_trace) cudaFree(c->chain_trace);
   delete c;
 }

@@ -82,6 +82,15 @@ struct mg_ctx {
   int chain_trace_layer = -2;
   int chain_pf = 0;
   int fast_sk_override = 0;  // MG_FAST_SK (measurement)
+  int verify_mode = 0;       // mg_verify_mode (mg_set_policy)
+  uint8_t* pend_d = nullptr;  // [max_slots] pipelined verification: tentative token pending
+  int32_t* rank_slot_d = nullptr;
+  int32_t *mx_slot, *mx_pos, *mx_tok, *mx_nk;  // mixed token list [Tmax]
+  uint16_t* xlm = nullptr;   // LM-head input rows [2 * max_batch][d]
+  int32_t* fpin = nullptr;   // pinned readback of a pipelined step: ctrl | last | pos | shadow | pend
+  cudaEvent_t fev = nullptr;
+  bool f_sync = false;       // a pipelined step's readback is in flight
+  std::vector<char> pend_h;
   int fast_mode = 0;         // mg_fast_schedule (mg_set_policy)
   int repair_mode = 0;       // mg_repair_action
   int det_sk = 512;          // verifier attention keys per split (A14; MG_DET_SK for measurement)  // chain L2 run-ahead (k-blocks per CTA; measured harmful, off)

@@ -139,6 +139,7 @@ struct QkvArgs {
   const uint16_t* bias;  // nullable
   const int32_t* pos;
   int T, H, KV, hd;
+  int part_T;            // rows of the partial buffer (slot stride); 0 = T
   const float* rcos;
   const float* rsin;
   uint16_t* q;
@@ -216,7 +217,7 @@ __device__ __forceinline__ QkvPair qkv_prep_staged(const QkvArgs& a, int t, int 
 }
 __device__ __forceinline__ void qkv_finish(const QkvArgs& a, const QkvPair& r, const float* part, const PartSpec& ps,
                                            int h, int i) {
-  const size_t stride = (size_t)a.T * (a.H + 2 * a.KV) * a.hd;
+  const size_t stride = (size_t)(a.part_T ? a.part_T : a.T) * (a.H + 2 * a.KV) * a.hd;
   float x = sum_splits(part, part_count(ps, r.f1), stride, r.row + r.f1);
   float y = sum_splits(part, part_count(ps, r.f2), stride, r.row + r.f2);
   if (a.bias) {

@@ -90,7 +90,7 @@ cudaError_t launch_rmsnorm(const uint16_t* x, const uint16_t* w, int T, int d, f
 cudaError_t launch_epi_qkv(const float* part, PartSpec ps, const uint16_t* bias, const int32_t* pos, int T, int H,
                            int KV, int hd, const float* rope_cos, const float* rope_sin, uint16_t* q,
                            const CacheView* cache, const int32_t* slot, uint16_t* k_out, uint16_t* v_out,
-                           cudaStream_t st);
+                           cudaStream_t st, int part_T = 0 /* partial rows (slot stride); 0 = T */);
 cudaError_t launch_epi_residual(const uint16_t* x, const float* part, PartSpec ps, int T, int N, uint16_t* out,
                                 cudaStream_t st);
 // x <- bf16(x + sum_s part[s]); xn <- RMSNorm(x, w) (xn nullable)
@@ -137,6 +137,11 @@ struct AttnArgs {
   const int32_t* pos;     // [T] (= n_keys - 1)
   const float* rcos;      // RoPE tables [max_pos][hd/2]
   const float* rsin;
+  // mixed launches (fast rows + verifier rows in one GEMM pass, engine.cu
+  // forward_mixed): rows of the QKV partial buffer (0 = T) and the q-row
+  // offset of this launch's token 0 in the Q tensor map
+  int32_t part_T;
+  int32_t q_row0;
 };
 bool make_tmap_3d(CUtensorMap* m, const void* base, int d0, int64_t d1, int64_t d2, int box1);
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st);

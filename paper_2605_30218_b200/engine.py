@@ -15,6 +15,8 @@ from ._lib import MgBuffers, MgConfig, MgSizes, MgStats, check, lib
 KIND_FAST, KIND_VERIFIED, KIND_REPAIR = 0, 1, 2
 FAST_BATCH_SHAPED, FAST_BATCH_INVARIANT = 0, 1   # mg_fast_schedule
 REPAIR_COLUMN, REPAIR_TOKEN_ONLY = 0, 1         # mg_repair_action
+VERIFY_SYNC, VERIFY_PIPELINED = 0, 1            # mg_verify_mode
+KIND_TENTATIVE, KIND_REPLACE = 3, 4             # pipelined-mode kinds
 
 
 def make_config(shape: dict, max_batch: int, max_slots: int, max_seq: int, page_size: int = 64,
@@ -83,11 +85,17 @@ class Engine:
         d["nan"] = st == _lib.MG_ERR_NUMERIC
         return d
 
-    def set_policy(self, fast_schedule: int = 0, repair_action: int = 0):
+    def set_policy(self, fast_schedule: int | None = None, repair_action: int | None = None,
+                   verify_mode: int | None = None):
         """mg_set_policy: fast_schedule 0 batch-shaped (default) / 1 batch-invariant
         (PAPER.md:227 global baseline); repair_action 0 column /
-        1 token-only ablation."""
-        check(lib().mg_set_policy(self.ctx, int(fast_schedule), int(repair_action)), self.ctx, "mg_set_policy")
+        1 token-only ablation; verify_mode 0 sync / 1 pipelined
+        (include/mg.h MG_VERIFY_PIPELINED: kinds 3 tentative, 4 replace).
+        None keeps the current value."""
+        cur = getattr(self, "_policy", (0, 0, 0))
+        new = tuple(int(v) if v is not None else c for v, c in zip((fast_schedule, repair_action, verify_mode), cur))
+        check(lib().mg_set_policy(self.ctx, *new), self.ctx, "mg_set_policy")
+        self._policy = new
 
     def verify_window(self, slots):
         """mg_verify_window (LLM-42-style verify + rollback, PAPER.md:227, 251,

@@ -10,6 +10,10 @@
   bit-identical across batch sizes and equals the tau=inf run.
 * NEXT-3 repair-action ablation: token-only repair keeps the
   BF16 column; under reading A1 tau=inf still emits the reference.
+* Pipelined verification (MG_VERIFY_PIPELINED, include/mg.h): the gated rows'
+  verifier rides on the next step's weight pass; the committed sequences are
+  bit-identical to the synchronous mode's (a row's fast path does not depend
+  on the other rows), with and without the long-catch-up fallback.
 """
 import numpy as np
 import pytest
@@ -195,8 +199,9 @@ def test_policy_and_window_errors(torch, tiny):
     shp, _ = tiny
     eng = _engine(shp, 2)
     L = _lib.lib()
-    assert L.mg_set_policy(eng.ctx, 2, 0) == _lib.MG_ERR_INVALID
-    assert L.mg_set_policy(eng.ctx, 0, 7) == _lib.MG_ERR_INVALID
+    assert L.mg_set_policy(eng.ctx, 2, 0, 0) == _lib.MG_ERR_INVALID
+    assert L.mg_set_policy(eng.ctx, 0, 7, 0) == _lib.MG_ERR_INVALID
+    assert L.mg_set_policy(eng.ctx, 0, 0, 5) == _lib.MG_ERR_INVALID
     s = np.array([0], np.int32)
     assert L.mg_verify_window(eng.ctx, s.ctypes.data, 1, None, None, None) == _lib.MG_ERR_INVALID  # inactive
     eng.prefill(0, [1, 2, 3])
@@ -206,4 +211,74 @@ def test_policy_and_window_errors(torch, tiny):
     # nothing unverified: a no-op that reports the current position
     pos, last, rb = eng.verify_window([0])
     assert pos[0] == 3 and rb[0] == 0
+    eng.close()
+
+
+def _pipelined(torch, eng, prompts, steps, tau, prot=None, recs=None):
+    """Pipelined decode: kinds 0/1/3 append, kind 4 replaces the slot's last
+    token (include/mg.h).  Ends with mg_verify_window to resolve the last
+    tentative tokens."""
+    from paper_2605_30218_b200.engine import VERIFY_PIPELINED
+    B = len(prompts)
+    eng.set_policy(verify_mode=VERIFY_PIPELINED)
+    seqs = [[eng.prefill(i, p)] for i, p in enumerate(prompts)]
+    out = torch.empty(B, dtype=torch.int32, device="cuda")
+    kind = torch.empty(B, dtype=torch.uint8, device="cuda")
+    for _ in range(steps - 1):
+        eng.step(list(range(B)), prot, tau, out, kind)
+        o, k = out.cpu().numpy(), kind.cpu().numpy()
+        if recs is not None:
+            recs.append(k.copy())
+        for b in range(B):
+            if k[b] == 4:
+                seqs[b][-1] = int(o[b])
+            else:
+                seqs[b].append(int(o[b]))
+    pos, last, rb = eng.verify_window(list(range(B)))
+    for b in range(B):
+        n = int(pos[b]) - len(prompts[b]) + 1
+        del seqs[b][n:]
+        seqs[b][-1] = int(last[b])
+    return seqs
+
+
+@pytest.mark.parametrize("tau,prot_mode,vc", [(INF, "all", 0), (0.3, "half", 0), (0.3, "all", 16), (INF, "all", 16)])
+def test_pipelined_equals_sync(torch, tiny, tau, prot_mode, vc):
+    shp, _ = tiny
+    B, steps = 6, 40
+    prompts = inputs.prompts(B, inputs.ragged_lengths(B, 8, 23, seed=41), shp["vocab"], seed=350)
+    prot = inputs.protected_mask(B, prot_mode)
+    ref = _decode(torch, _engine(shp, B, verify_chunk=vc), prompts, steps, tau, prot)
+    eng = _engine(shp, B, verify_chunk=vc)
+    recs = []
+    got = _pipelined(torch, eng, prompts, steps, tau, prot, recs)
+    st = eng.stats()
+    for b in range(B):
+        n = min(len(got[b]), len(ref[b]))
+        assert n >= steps // 2
+        assert got[b][:n] == ref[b][:n], b
+    kinds = np.array(recs)
+    assert (kinds == 4).sum() == st["repairs"]
+    assert st["triggers"] >= st["verified"] + st["repairs"]
+    if tau == INF:
+        assert (kinds == 3).all() or ((kinds == 3) | (kinds == 4)).all()
+    eng.close()
+
+
+def test_pipelined_errors(torch, tiny):
+    from paper_2605_30218_b200 import _lib
+    shp, _ = tiny
+    eng = _engine(shp, 2)
+    eng.set_policy(verify_mode=1)
+    for i in range(2):
+        eng.prefill(i, [3 + i, 4, 5, 6])
+    out = torch.empty(2, dtype=torch.int32, device="cuda")
+    eng.step([0, 1], None, INF, out)          # both rows tentative now
+    from paper_2605_30218_b200._lib import MgError
+    with pytest.raises(MgError):
+        eng.step([0], None, INF, out)         # slot 1 pending but missing
+    L = _lib.lib()
+    assert L.mg_set_policy(eng.ctx, 0, 0, 0) == _lib.MG_ERR_STATE
+    eng.verify_window([0, 1])
+    assert L.mg_set_policy(eng.ctx, 0, 0, 0) == _lib.MG_OK
     eng.close()
