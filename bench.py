@@ -528,7 +528,7 @@ def cpu_baseline(args, shp, tau):
     if avail and avail < need:
         return {"value": None, "unit": "tok/s", "cores": cores, "kind": "oracle",
                 "sample": f"skipped: {avail / 2**30:.0f} GiB host RAM < {need / 2**30:.0f} GiB needed"}
-    n, dt = _oracle_sample(shp, 8, 2, tau, 60.0)
+    n, dt = _oracle_sample(shp, 8, 8, tau, 25.0)   # ~10-30 s of CPU work
     return {"value": round(n / dt, 5), "unit": "tok/s", "cores": cores, "kind": "oracle",
             "sample": f"{args.model}-shaped, 1 row, {n} MarginGate decode steps (tau={tau}) after an 8-token "
                       f"deterministic prefill; {dt:.1f} s of CPU time"}
