@@ -434,7 +434,10 @@ def run_gpu(args):
                      "gemm_us_per_launch": round(1e3 * tim["gemm_ms"] / max(tim["gemm_launches"], 1), 2),
                      "gemm_ms_per_step": round(tim["gemm_ms"] / K, 4),
                      "attn_ms_per_step": round(tim["attn_ms"] / K, 4),
-                     "fast_step_ms_timed_pass": round(tim["step_ms"] / max(tim["steps"], 1), 4)},
+                     "fast_step_ms_timed_pass": round(tim["step_ms"] / max(tim["steps"], 1), 4),
+                     # the whole pipelined BF16 step (CUDA graph, PDL) against the same peak:
+                     # algorithmic bytes = weights once + every row's K/V context
+                     "step": _step_roofline(shp, B, ctx0 + W + K // 2, T["bf16"] / K, hbm)},
         "e2e": {"value": round(tok / (t_e2e * 1e-3), 2), "unit": "tok/s", "h2d_bytes_per_step": B * 5,
                 "d2h_bytes_per_step": B * 5},
         "gpu_launches": res["mg"]["launches"],
@@ -490,6 +493,19 @@ def run_gpu(args):
     if ws > 1:
         dist.destroy_process_group()
     return line
+
+
+def _step_roofline(shp, B, ctx, ms, peak_gbs):
+    """SURVEY 8(d) per-step algorithmic bytes of the fast path: every weight
+    streamed once (QKV, O, gate/up, down per layer + LM head) + each row's K/V
+    over `ctx` keys; achieved = bytes / measured ms per step."""
+    L, d, H, KV, hd, F, V = (shp[k] for k in ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "d_ff",
+                                                "vocab"))
+    w = 2 * (L * ((H + 2 * KV) * hd * d + d * H * hd + 3 * F * d) + V * d)
+    kv = B * ctx * L * 2 * KV * hd * 2
+    gbs = (w + kv) / (ms * 1e-3) / 1e9
+    return {"bytes": w + kv, "weights": w, "kv": kv, "ms": round(ms, 4), "achieved": round(gbs, 1),
+            "frac": round(gbs / peak_gbs, 4)}
 
 
 def _oracle_sample(shp, prompt_len, steps, tau, budget_s):

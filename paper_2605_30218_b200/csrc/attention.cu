@@ -22,10 +22,10 @@
 // a function of (n_keys, split_keys) alone, so with a pinned split_keys (the
 // verifier) a query's result does not depend on the batch.
 //
-// Data movement: TMA only.  Each warp owns a ring of R stages (K block + V
-// block, box 64 dims x 16 keys, 128B swizzle -> conflict-free ldmatrix) that
-// its lane 0 refills as soon as the warp has consumed a stage; warp 0 loads
-// the Q tile once.  On the fast path (prewait) the first blocks, which hold
+// Data movement: TMA only.  Each warp owns a ring of RK K blocks and one of RV
+// V blocks (box 64 dims x 16 keys, 128B swizzle -> conflict-free ldmatrix);
+// its lane 0 refills a K stage right after QK^T has read it and a V stage
+// right after PV; warp 0 loads the Q tile once.  On the fast path (prewait) the first blocks, which hold
 // only keys of earlier steps, are requested before griddepcontrol.wait, so
 // their latency overlaps the tail of the QKV epilogue.  Page-table lookups for 32 blocks at a time are done by the
 // 32 lanes in parallel and shuffled to lane 0 at issue time.
@@ -39,20 +39,25 @@ namespace mg {
 
 constexpr int kAtThreads = 128;
 
-template <int HD, int R>
+// Per warp: a ring of RK K blocks and a separate ring of RV V blocks, each
+// with its own mbarriers, so the K block of step i + RK is requested as soon as
+// QK^T of step i has read its stage (it streams while softmax and PV run) and
+// the V block of step i + RV as soon as PV of step i is done.
+template <int HD, int RK, int RV>
 struct AtCfg {
   static constexpr int HALVES = HD / 64;
   static constexpr int BLK = HALVES * 2048;        // one 16-row tile: HALVES x [16][128 B] swizzled
-  static constexpr int STAGE = 2 * BLK;            // K block + V block
+  static constexpr int WRING = (RK + RV) * BLK;    // one warp's K ring then V ring
   static constexpr int XST = HD + 8;               // cross-warp scratch row stride (floats)
-  static constexpr int RING = 4 * R * STAGE;
+  static constexpr int RING = 4 * WRING;
   static constexpr int XG = 4 * 16 * XST * 4;      // [warp][16][XST] fp32, aliases the rings
   static constexpr int Q_OFF = 0;
   static constexpr int RING_OFF = BLK;
   static constexpr int ML_OFF = RING_OFF + (RING > XG ? RING : XG);  // m, l: [warp][16] each
   static constexpr int KVN_OFF = ML_OFF + 2 * 64 * 4;                // fused QKV: new K and V rows [2][HD] bf16
-  static constexpr int BAR_OFF = KVN_OFF + 2 * HD * 2;                // Q, then [warp][R]
-  static constexpr int SMEM = BAR_OFF + (1 + 4 * R) * 8 + 8 + 1024;   // + flag + alignment slack
+  static constexpr int NBAR = 1 + 4 * (RK + RV);                     // Q, then [warp][RK K | RV V]
+  static constexpr int BAR_OFF = KVN_OFF + 2 * HD * 2;
+  static constexpr int SMEM = BAR_OFF + NBAR * 8 + 8 + 1024;         // + flag + alignment slack
 };
 
 MG_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -83,21 +88,21 @@ MG_DEV void split_pair(float e0, float e1, uint32_t& hi, uint32_t& lo) {
   lo = pack_bf2(__fsub_rn(e0, lo_bf(hi)), __fsub_rn(e1, hi_bf(hi)));
 }
 
-template <int HD, int R>
+template <int HD, int RK, int RV>
 __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ AttnArgs a) {
-  using C = AtCfg<HD, R>;
+  using C = AtCfg<HD, RK, RV>;
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
   float* s_m = reinterpret_cast<float*>(sm + C::ML_OFF);  // [warp][16]
   float* s_l = s_m + 64;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
-  int* s_flag = reinterpret_cast<int*>(bars + 1 + 4 * R);
+  int* s_flag = reinterpret_cast<int*>(bars + C::NBAR);
 
   const int t = blockIdx.x, kvh = blockIdx.y, sp = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.H, G = a.H / a.KV;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 1 + 4 * R; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < C::NBAR; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -109,52 +114,65 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
   const int nblk = (hi - lo + 15) >> 4;
   const int nbw = nblk > warp ? (nblk - warp + 3) >> 2 : 0;  // blocks of this warp
   const int n_sp = (n + a.split_keys - 1) / a.split_keys;
-  uint8_t* ring = sm + C::RING_OFF + warp * R * C::STAGE;
-  uint64_t* full = bars + 1 + warp * R;
+  uint8_t* kring = sm + C::RING_OFF + warp * C::WRING;
+  uint8_t* vring = kring + RK * C::BLK;
+  uint64_t* kfull = bars + 1 + warp * (RK + RV);
+  uint64_t* vfull = kfull + RK;
 
-  // ---- TMA issue: Q tile (warp 0), then the first R blocks of each warp
-  int my_sl = 0, my_row = 0;  // lane j: coordinates of this warp's block (32*batch + j)
-  auto coords = [&](int base) {
+  // ---- TMA issue: Q tile (warp 0), then the first RK K / RV V blocks of each warp.
+  // Lane j caches the page coordinates of block (32*batch + j); the K and V
+  // streams advance at different times and keep one cache each.
+  int k_sl = 0, k_row = 0, v_sl = 0, v_row = 0;
+  auto coords = [&](int base, int& o_sl, int& o_row) {
     const int i = base + lane;
     if (i < nbw) {
       const int key0 = lo + 16 * (warp + 4 * i);
       if (a.paged) {
         const CacheView& cv = a.cache;
         const int page = cv.pt[(size_t)a.slot[t] * cv.max_pages + key0 / cv.page_size];
-        my_sl = (cv.layer * cv.n_pages + page) * 2 * a.KV + kvh;
-        my_row = key0 % cv.page_size;
+        o_sl = (cv.layer * cv.n_pages + page) * 2 * a.KV + kvh;
+        o_row = key0 % cv.page_size;
       } else {
-        my_sl = t * a.KV + kvh;
-        my_row = key0;
+        o_sl = t * a.KV + kvh;
+        o_row = key0;
       }
     }
   };
   const int vsl = a.paged ? a.KV : 0;  // V slab offset inside the pool map
-  auto issue = [&](int i) {            // warp-wide (shuffles); lane 0 issues
-    const int sl = __shfl_sync(0xffffffffu, my_sl, i & 31), row = __shfl_sync(0xffffffffu, my_row, i & 31);
+  auto issue_k = [&](int i) {          // warp-wide (shuffles); lane 0 issues
+    const int sl = __shfl_sync(0xffffffffu, k_sl, i & 31), row = __shfl_sync(0xffffffffu, k_row, i & 31);
     if (lane == 0) {
-      const int s = i % R;
-      uint8_t* st = ring + s * C::STAGE;
-      mbar_expect_tx(&full[s], C::STAGE);
-#pragma unroll
-      for (int h = 0; h < C::HALVES; ++h) tma_load_3d(st + h * 2048, &a.kmap, &full[s], 64 * h, row, sl);
+      const int s = i % RK;
+      mbar_expect_tx(&kfull[s], C::BLK);
 #pragma unroll
       for (int h = 0; h < C::HALVES; ++h)
-        tma_load_3d(st + C::BLK + h * 2048, &a.vmap, &full[s], 64 * h, row, sl + vsl);
+        tma_load_3d(kring + s * C::BLK + h * 2048, &a.kmap, &kfull[s], 64 * h, row, sl);
     }
   };
-  coords(0);
-  int issued = 0;
+  auto issue_v = [&](int i) {
+    const int sl = __shfl_sync(0xffffffffu, v_sl, i & 31), row = __shfl_sync(0xffffffffu, v_row, i & 31);
+    if (lane == 0) {
+      const int s = i % RV;
+      mbar_expect_tx(&vfull[s], C::BLK);
+#pragma unroll
+      for (int h = 0; h < C::HALVES; ++h)
+        tma_load_3d(vring + s * C::BLK + h * 2048, &a.vmap, &vfull[s], 64 * h, row, sl + vsl);
+    }
+  };
+  coords(0, k_sl, k_row);
+  v_sl = k_sl;
+  v_row = k_row;
+  int ik = 0, iv = 0;  // blocks issued per stream
   if (a.prewait) {
     // PDL: blocks whose keys all precede this step's appended column (n - 1)
     // were written by earlier steps -- fetched before griddepcontrol.wait
-    for (; issued < R && issued < nbw; ++issued) {
-      if (lo + 16 * (warp + 4 * issued) + 16 > n - 1) break;
-      issue(issued);
-    }
+    auto early = [&](int i) { return lo + 16 * (warp + 4 * i) + 16 <= n - 1; };
+    for (; ik < RK && ik < nbw && early(ik); ++ik) issue_k(ik);
+    for (; iv < RV && iv < nbw && early(iv); ++iv) issue_v(iv);
     griddep();
   }
-  for (int i = issued; i < R && i < nbw; ++i) issue(i);  // the remaining first blocks (after the wait)
+  for (; ik < RK && ik < nbw; ++ik) issue_k(ik);  // the remaining first blocks (after the wait)
+  for (; iv < RV && iv < nbw; ++iv) issue_v(iv);
   uint16_t* kvn = reinterpret_cast<uint16_t*>(sm + C::KVN_OFF);
   const bool has_new = a.fuse_qkv && sp == n_sp - 1;  // this CTA holds key n - 1
   if (!a.fuse_qkv) {
@@ -225,25 +243,16 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
   for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows r0, r1 (l: this lane's keys)
   for (int i = 0; i < nbw; ++i) {
-    const int s = i % R;
-    mbar_wait(&full[s], (uint32_t)((i / R) & 1));
-    uint8_t* st = ring + s * C::STAGE;
-    const uint32_t kb = smem_u32(st), vb = kb + C::BLK;
+    uint8_t* kst = kring + (i % RK) * C::BLK;
+    uint8_t* vst = vring + (i % RV) * C::BLK;
+    const uint32_t kb = smem_u32(kst), vb = smem_u32(vst);
     const int valid = min(16, hi - (lo + 16 * (warp + 4 * i)));
-    if (valid < 16) {  // the split's last block: zero V rows past the end (P is 0 there)
-      for (int e = lane; e < (16 - valid) * C::HALVES * 8; e += 32) {
-        const int row = valid + e / (C::HALVES * 8), rem = e % (C::HALVES * 8);
-        reinterpret_cast<uint4*>(st + C::BLK + (rem >> 3) * 2048 + row * 128)[rem & 7] = make_uint4(0, 0, 0, 0);
-      }
-      __syncwarp();
-    }
-    if (has_new && lo + 16 * (warp + 4 * i) + 16 >= n) {  // the block holding key n - 1: patch its K/V row
-      const int rr = n - 1 - (lo + 16 * (warp + 4 * i));
-      for (int e = lane; e < 2 * (HD / 8); e += 32) {
-        const int sel = e / (HD / 8), col = (e % (HD / 8)) * 8;
-        *reinterpret_cast<uint4*>(st + sel * C::BLK + swz(rr, col)) =
-            *reinterpret_cast<const uint4*>(kvn + sel * HD + col);
-      }
+    const bool new_blk = has_new && lo + 16 * (warp + 4 * i) + 16 >= n;  // holds key n - 1
+    const int rr_new = n - 1 - (lo + 16 * (warp + 4 * i));
+    mbar_wait(&kfull[i % RK], (uint32_t)((i / RK) & 1));
+    if (new_blk) {  // patch the new K row
+      for (int e = lane; e < HD / 8; e += 32)
+        *reinterpret_cast<uint4*>(kst + swz(rr_new, e * 8)) = *reinterpret_cast<const uint4*>(kvn + e * 8);
       __syncwarp();
     }
     // scores: two 8-key tiles
@@ -293,6 +302,26 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
       acc[nt][2] = __fmul_rn(acc[nt][2], al1);
       acc[nt][3] = __fmul_rn(acc[nt][3], al1);
     }
+    // the K stage is consumed: stream the K block RK steps ahead during softmax + PV
+    if (i + RK < nbw) {
+      __syncwarp();
+      fence_proxy_async();
+      if (((i + RK) & 31) == 0) coords(i + RK, k_sl, k_row);
+      issue_k(i + RK);
+    }
+    mbar_wait(&vfull[i % RV], (uint32_t)((i / RV) & 1));
+    if (valid < 16) {  // the split's last block: zero V rows past the end (P is 0 there)
+      for (int e = lane; e < (16 - valid) * C::HALVES * 8; e += 32) {
+        const int row = valid + e / (C::HALVES * 8), rem = e % (C::HALVES * 8);
+        reinterpret_cast<uint4*>(vst + (rem >> 3) * 2048 + row * 128)[rem & 7] = make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+    }
+    if (new_blk) {  // patch the new V row
+      for (int e = lane; e < HD / 8; e += 32)
+        *reinterpret_cast<uint4*>(vst + swz(rr_new, e * 8)) = *reinterpret_cast<const uint4*>(kvn + HD + e * 8);
+      __syncwarp();
+    }
     uint32_t ph[4], pl[4];
     split_pair(e[0][0], e[0][1], ph[0], pl[0]);  // row r0, keys cc, cc+1
     split_pair(e[0][2], e[0][3], ph[1], pl[1]);  // row r1, keys cc, cc+1
@@ -307,11 +336,11 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
       mma_bf16(acc[2 * n2 + 1], ph, b2, b3);
       mma_bf16(acc[2 * n2 + 1], pl, b2, b3);
     }
-    if (i + R < nbw) {  // refill the stage just consumed
+    if (i + RV < nbw) {  // refill the V stage just consumed
       __syncwarp();
       fence_proxy_async();
-      if (((i + R) & 31) == 0) coords(i + R);
-      issue(i + R);
+      if (((i + RV) & 31) == 0) coords(i + RV, v_sl, v_row);
+      issue_v(i + RV);
     }
   }
   // lane partial sums -> row sums (fixed butterfly, the same in all 4 lanes)
@@ -392,21 +421,25 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
   }
 }
 
-template <int HD, int R>
+template <int HD, int RK, int RV>
 static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k_attn<HD, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, AtCfg<HD, R>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_attn<HD, RK, RV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         AtCfg<HD, RK, RV>::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_k(k_attn<HD, R>, dim3(a.T, a.KV, a.n_splits), dim3(kAtThreads), AtCfg<HD, R>::SMEM, st, a);
+  return launch_k(k_attn<HD, RK, RV>, dim3(a.T, a.KV, a.n_splits), dim3(kAtThreads), AtCfg<HD, RK, RV>::SMEM, st,
+                  a);
 }
 
-// ring depth: 2 stages per warp while the grid fits ~3 CTAs per SM, else 1
-// (more CTAs resident; the other warps of the SM cover the latency).
-// MG_ATTN_RING=1|2 forces it (measurement only).
+// ring depths (RK, RV): (2, 2) while the grid fits ~3 CTAs per SM; else
+// (1, 1) (4 CTAs per SM, 40 KB each at hd 128).  (2, 1) -- the K stream two
+// blocks ahead at 55 KB per CTA, still 4 per SM -- measured the same step time
+// at B = 64 / 8 (llama8b, ctx 384: 4.34 vs 4.33 ms, 3.48 vs 3.49 ms), so the
+// smaller footprint stays the default.  MG_ATTN_RING=11|21|22 forces it
+// (measurement only).
 static int g_attn_ring = 0;
 
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st) {
@@ -414,12 +447,17 @@ cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st) {
     return cudaErrorInvalidValue;
   if (!g_attn_ring) {
     const char* s = getenv("MG_ATTN_RING");
-    g_attn_ring = s && (atoi(s) == 1 || atoi(s) == 2) ? atoi(s) : -1;
+    const int v = s ? atoi(s) : 0;
+    g_attn_ring = (v == 11 || v == 21 || v == 22) ? v : -1;
   }
   const long ctas = (long)a.T * a.KV * a.n_splits;
-  const int R = g_attn_ring > 0 ? g_attn_ring : (ctas <= 3L * num_sms() ? 2 : 1);
-  if (a.hd == 128) return R == 2 ? launch_attn_t<128, 2>(a, st) : launch_attn_t<128, 1>(a, st);
-  if (a.hd == 64) return R == 2 ? launch_attn_t<64, 2>(a, st) : launch_attn_t<64, 1>(a, st);
+  const int R = g_attn_ring > 0 ? g_attn_ring : (ctas <= 3L * num_sms() ? 22 : 11);
+  if (a.hd == 128)
+    return R == 22 ? launch_attn_t<128, 2, 2>(a, st)
+                   : (R == 21 ? launch_attn_t<128, 2, 1>(a, st) : launch_attn_t<128, 1, 1>(a, st));
+  if (a.hd == 64)
+    return R == 22 ? launch_attn_t<64, 2, 2>(a, st)
+                   : (R == 21 ? launch_attn_t<64, 2, 1>(a, st) : launch_attn_t<64, 1, 1>(a, st));
   return cudaErrorInvalidValue;
 }
 
