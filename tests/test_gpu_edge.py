@@ -1,0 +1,126 @@
+"""Edge cases of the CUDA path through the C ABI (SURVEY 8(c) parity protocol):
+the ABI's maximum batch (256 rows, token tiles up to 256 columns and, in the
+pipelined mode, 512 GEMM columns), one-token prompts, ragged lengths that
+cross pages, and sampled rows checked against the oracle / against batch 1.
+"""
+import numpy as np
+import pytest
+
+from paper_2605_30218_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+BAND = 2 * TOL
+INF = float("inf")
+B_MAX = 256
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    return torch
+
+
+@pytest.fixture(scope="module")
+def tiny(orc):
+    shp = inputs.shape("tiny")
+    return shp, orc.Model(shp)
+
+
+def _engine(shape, B, max_seq=64):
+    from paper_2605_30218_b200.engine import Engine
+    return Engine(shape, max_batch=B, max_slots=B, max_seq=max_seq, page_size=16)
+
+
+def _prompts(shp):
+    lens = inputs.ragged_lengths(B_MAX, 1, 40, seed=77)
+    lens[0] = 1                      # a one-token prompt
+    return inputs.prompts(B_MAX, lens, shp["vocab"], seed=5000)
+
+
+def _decode(torch, eng, prompts, steps, tau, pipelined=False):
+    B = len(prompts)
+    if pipelined:
+        eng.set_policy(verify_mode=1)
+    seqs = [[eng.prefill(i, p)] for i, p in enumerate(prompts)]
+    out = torch.empty(B, dtype=torch.int32, device="cuda")
+    kind = torch.empty(B, dtype=torch.uint8, device="cuda")
+    for _ in range(steps - 1):
+        eng.step(list(range(B)), None, tau, out, kind)
+        o, k = out.cpu().numpy(), kind.cpu().numpy()
+        for b in range(B):
+            if pipelined and k[b] == 4:
+                seqs[b][-1] = int(o[b])
+            else:
+                seqs[b].append(int(o[b]))
+    if pipelined:
+        pos, last, _ = eng.verify_window(list(range(B)))
+        for b in range(B):
+            n = int(pos[b]) - len(prompts[b]) + 1
+            del seqs[b][n:]
+            seqs[b][-1] = int(last[b])
+    return seqs
+
+
+def test_max_batch_verifier_invariance(torch, tiny):
+    """tau=inf at the maximum batch: sampled rows bit-identical to batch 1,
+    and the pipelined mode (256 fast + 256 verifier GEMM columns) gives the
+    same sequences."""
+    shp, _ = tiny
+    prompts = _prompts(shp)
+    steps = 6
+    eng = _engine(shp, B_MAX)
+    full = _decode(torch, eng, prompts, steps, INF)
+    st = eng.stats()
+    assert st["triggers"] == B_MAX * (steps - 1)
+    eng.close()
+    for row in (0, 97, 255):
+        e1 = _engine(shp, 1)
+        assert _decode(torch, e1, [prompts[row]], steps, INF)[0] == full[row], row
+        e1.close()
+    eng = _engine(shp, B_MAX)
+    pipe = _decode(torch, eng, prompts, steps, INF, pipelined=True)
+    eng.close()
+    for b in range(B_MAX):
+        n = min(len(pipe[b]), len(full[b]))
+        assert n >= steps - 2 and pipe[b][:n] == full[b][:n], b
+
+
+def test_max_batch_fast_logits_vs_oracle(orc, torch, tiny):
+    """tau=0 at batch 256 (256-column token tile): sampled rows' fast logits
+    within 2e-2 of the oracle teacher-forced on the GPU's tokens; the fast
+    argmax equal outside the band."""
+    shp, m = tiny
+    prompts = _prompts(shp)
+    V = shp["vocab"]
+    eng = _engine(shp, B_MAX)
+    cap = torch.empty((B_MAX, V), dtype=torch.float32, device="cuda")
+    eng.capture_logits(cap)
+    first = [eng.prefill(i, p) for i, p in enumerate(prompts)]
+    out = torch.empty(B_MAX, dtype=torch.int32, device="cuda")
+    rows = (0, 131, 254)
+    toks = {r: [first[r]] for r in rows}
+    logits = {r: [] for r in rows}
+    for _ in range(3):
+        eng.step(list(range(B_MAX)), None, 0.0, out)
+        o = out.cpu().numpy()
+        lg = cap.cpu().numpy()
+        for r in rows:
+            toks[r].append(int(o[r]))
+            logits[r].append(lg[r].copy())
+    eng.close()
+    det = orc.det_sched()
+    for r in rows:
+        st = orc.State(m, 1, len(prompts[r]) + 8)
+        if st.prefill(0, prompts[r], det) != toks[r][0]:
+            st.close()
+            continue  # first token inside the ambiguity band
+        for t in range(3):
+            rr = st.step([0], [0], 0.0, orc.fast_sched(B_MAX), det, forced_out=[toks[r][t + 1]],
+                         forced_kind=[0], want_logits=True)
+            e = np.abs(logits[r][t] - rr["logits"][0])
+            assert np.quantile(e, 0.999) <= TOL and e.max() <= 1.5 * TOL, (r, t, float(e.max()))
+            if rr["g"][0] > 2 * e.max():
+                assert toks[r][t + 1] == int(rr["f_tok"][0])
+        st.close()
