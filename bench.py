@@ -179,7 +179,7 @@ def run_gpu(args):
     keys = ["steps", "rows", "protected_rows", "triggers", "verified", "repairs", "verifier_launches",
             "catchup_tokens"]
 
-    def run_arm(tau, prot, timing=False, clocks=None, pipelined=False):
+    def run_arm(tau, prot, timing=False, clocks=None, pipelined=False, fused=False):
         """Fresh deterministic prefill, W warm-up steps, K timed steps (CUDA events
         on the engine's stream, barrier + synchronize on both sides).
         pipelined: MG_VERIFY_PIPELINED (include/mg.h) -- a gated row's
@@ -189,7 +189,7 @@ def run_gpu(args):
                 eng.release(i)
             except Exception:
                 pass
-        eng.set_policy(verify_mode=1 if pipelined else 0)
+        eng.set_policy(verify_mode=1 if pipelined else (2 if fused else 0))
         first = [eng.prefill(i, p) for i, p in enumerate(prompts)]
         s0 = eng.stats()
         toks, kinds_w = [], []
@@ -244,6 +244,8 @@ def run_gpu(args):
                 del seqs[b][n:]
                 seqs[b][-1] = int(last[b])
             eng.set_policy(verify_mode=0)
+        if fused:
+            eng.set_policy(verify_mode=0)
         r["seqs"] = seqs
         r["tokens"] = int(B * K - (kt == 4).sum()) if pipelined else B * K
         r["stats"] = {k: s1[k] - s0[k] for k in keys}
@@ -266,12 +268,16 @@ def run_gpu(args):
     # pipelined verification (include/mg.h MG_VERIFY_PIPELINED): always-on with the
     # verifier riding on the next step's weight pass
     res["ao_pipe"] = run_arm(math.inf, head, pipelined=True)
+    # fused same-step verification (MG_VERIFY_FUSED): synchronous semantics, one weight pass
+    res["mg_fused"] = run_arm(tau, head, fused=True)
+    res["ao_fused"] = run_arm(math.inf, head, fused=True)
     other = "all" if args.protected == "one" else "one"
     if not args.quick:
         po = prot_all if other == "all" else prot_one
         res["mg_other"] = run_arm(tau, po)
         res["ao_other"] = run_arm(math.inf, po)
         res["ao_pipe_other"] = run_arm(math.inf, po, pipelined=True)
+        res["ao_fused_other"] = run_arm(math.inf, po, fused=True)
     # dominant-kernel timing pass: the fast path with CUDA events around every
     # GEMM / attention launch (events break the PDL overlap, so this pass is
     # separate from the timed arms; the per-launch durations are what ncu's
@@ -327,6 +333,9 @@ def run_gpu(args):
         # pipelined verification (include/mg.h MG_VERIFY_PIPELINED)
         r8["margingate_pipelined"] = _decode_run(e8, ev8, t8, p1, W, K, timed=True, pipelined=True)
         r8["always_on_pipelined"] = _decode_run(e8, ev8, math.inf, p1, W, K, timed=True, pipelined=True)
+        # fused same-step verification (MG_VERIFY_FUSED)
+        r8["margingate_fused"] = _decode_run(e8, ev8, t8, p1, W, K, timed=True, fused=True)
+        r8["always_on_fused"] = _decode_run(e8, ev8, math.inf, p1, W, K, timed=True, fused=True)
         # NEXT-2 LLM-42 windowed verify + rollback, K = 64, over 2 windows
         win = _window_run(e8, ev8, p1, W, 2 * args.window, args.window)
         e8.close()
@@ -336,7 +345,8 @@ def run_gpu(args):
     def det(a, b, prot):
         return sum(1 for i in range(B) if prot[i] and res[a]["seqs"][i] == res[b]["seqs"][i]), int(prot.sum())
 
-    arms = [a for a in ("bf16", "mg", "ao", "ao_pipe", "mg_other", "ao_other", "ao_pipe_other") if a in res]
+    arms = [a for a in ("bf16", "mg", "ao", "ao_pipe", "mg_fused", "ao_fused", "mg_other", "ao_other", "ao_pipe_other",
+                        "ao_fused_other") if a in res]
     vec = []
     for a in arms:
         vec += [res[a]["stats"][k] for k in keys]
@@ -351,7 +361,8 @@ def run_gpu(args):
     dh = det("mg", "ao", head)
     do = det("mg_other", "ao_other", prot_all if other == "all" else prot_one) if "mg_other" in res else (0, 0)
     dp = det_prefix("ao_pipe", "ao", head)
-    vec += [*dh, *do, *dp, *[res[a]["tokens"] for a in arms]]
+    df = det("mg_fused", "ao_fused", head)
+    vec += [*dh, *do, *dp, *df, *[res[a]["tokens"] for a in arms]]
     times = [res[a]["ms"] for a in arms] + [e2e_ms]
     vec, times = sharding.aggregate(vec, times, device="cuda")
     if rank != 0:
@@ -359,8 +370,9 @@ def run_gpu(args):
             dist.destroy_process_group()
         return None
     stats = {a: dict(zip(keys, vec[i * len(keys):(i + 1) * len(keys)])) for i, a in enumerate(arms)}
-    dh, do, dp = vec[len(arms) * len(keys):][:2], vec[len(arms) * len(keys):][2:4], vec[len(arms) * len(keys):][4:6]
-    ntok = dict(zip(arms, vec[len(arms) * len(keys) + 6:]))
+    tail = vec[len(arms) * len(keys):]
+    dh, do, dp, df = tail[:2], tail[2:4], tail[4:6], tail[6:8]
+    ntok = dict(zip(arms, tail[8:]))
     T = dict(zip(arms, times[:-1]))
     t_e2e = times[-1]
     tok = ws * B * K
@@ -403,9 +415,21 @@ def run_gpu(args):
     if calib:
         arms_out["calibration"] = calib
     arms_out["headline"]["pipelined"] = pipe("ao_pipe", args.protected, dp)
+    arms_out["headline"]["fused"] = {
+        "margingate_tok_s": round(tok / (T["mg_fused"] * 1e-3), 2),
+        "always_on_tok_s": round(tok / (T["ao_fused"] * 1e-3), 2),
+        "inc_margingate": round(metrics.latency_increment(T["mg_fused"], T["bf16"]), 4),
+        "inc_always_on": round(metrics.latency_increment(T["ao_fused"], T["bf16"]), 4),
+        "trigger_pct": round(100 * metrics.rates(stats["mg_fused"])["r_verify"], 3),
+        "determinism_pct": round(100 * df[0] / df[1], 2) if df[1] else None,
+        "note": "MG_VERIFY_FUSED: every protected row's verifier token computed speculatively in the same "
+                "weight pass; the gate selects which to commit (synchronous semantics)"}
     if "mg_other" in res:
         arms_out["other"] = summary("mg_other", "ao_other", do, other)
         arms_out["other"]["pipelined"] = pipe("ao_pipe_other", other, None)
+        arms_out["other"]["fused"] = {
+            "always_on_tok_s": round(tok / (T["ao_fused_other"] * 1e-3), 2),
+            "inc_always_on": round(metrics.latency_increment(T["ao_fused_other"], T["bf16"]), 4)}
     arms_out["paper_context"] = ("A6000, bs=8, one protected request: 2.23x (8B) / 1.99x (14B) increment reduction "
                                  "at 18.56% / 15.05% triggers (PAPER.md:5, 285, 296) -- context, not the target")
     line = {
@@ -468,13 +492,14 @@ def run_gpu(args):
                                   "note": "repair-action ablation, PAPER.md:317"},
             "batch_invariant": {"inc": round(metrics.latency_increment(tm["batch_invariant"], tm["bf16"]), 4),
                                 "note": "global batch-invariant fast schedule at tau=0 (PAPER.md:227)"},
-            "pipelined": {n: {"inc": round((tm[n] / r8[n][1]["tokens"]) / (tm["bf16"] / (pb * K)) - 1, 4),
+            "verify_modes": {n: {"inc": round((tm[n] / r8[n][1]["tokens"]) / (tm["bf16"] / (pb * K)) - 1, 4),
                               "trigger_pct": round(100 * metrics.rates(r8[n][1])["r_verify"], 3),
                               "repairs": r8[n][1]["repairs"],
                               "protected_row_equals_reference_prefix":
                                   r8[n][0][0][:min(len(r8[n][0][0]), len(r8["always_on"][0][0]))] ==
                                   r8["always_on"][0][0][:min(len(r8[n][0][0]), len(r8["always_on"][0][0]))]}
-                          for n in ("margingate_pipelined", "always_on_pipelined")},
+                          for n in ("margingate_pipelined", "always_on_pipelined", "margingate_fused",
+                                    "always_on_fused")},
             "note": "rank 0's numbers (times not reduced over ranks)"}
         wseq, wtok, wms, wst = paper["window"]
         t_tok_bf16 = tm["bf16"] / (pb * K)
@@ -582,7 +607,7 @@ def run_reference(args):
             "e2e": {"value": round(v, 5), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
-def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False, flips=None, pipelined=False):
+def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False, flips=None, pipelined=False, fused=False):
     """Fresh prefill of `prompts`, W + K decode steps at threshold tau; eps (a
     list) collects eps_pert per (row, step) -- only valid at tau = inf with
     every row protected, where the verifier's rank k is row k.  flips (a
@@ -600,7 +625,7 @@ def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False, flips=None
             eng.release(i)
         except Exception:
             pass
-    eng.set_policy(verify_mode=1 if pipelined else 0)
+    eng.set_policy(verify_mode=1 if pipelined else (2 if fused else 0))
     seqs = [[eng.prefill(i, p)] for i, p in enumerate(prompts)]
     s0 = eng.stats()
     capf = capv = None
@@ -645,6 +670,8 @@ def _decode_run(eng, prompts, tau, prot, W, K, eps=None, timed=False, flips=None
             n = int(pos[b]) - len(prompts[b]) + 1
             del seqs[b][n:]
             seqs[b][-1] = int(last[b])
+        eng.set_policy(verify_mode=0)
+    if fused:
         eng.set_policy(verify_mode=0)
     s1 = eng.stats()
     st = {k: s1[k] - s0[k] for k in ("protected_rows", "triggers", "repairs")}

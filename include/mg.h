@@ -111,8 +111,17 @@ typedef enum { MG_REPAIR_COLUMN = 0, MG_REPAIR_TOKEN_ONLY = 1 } mg_repair_action
  *                        MG_VERIFY_SYNC ones (the fast path of a row does not
  *                        depend on the other rows).  A slot with a pending token
  *                        must be in the next batch (else MG_ERR_STATE) or be
- *                        resolved with mg_verify_window. */
-typedef enum { MG_VERIFY_SYNC = 0, MG_VERIFY_PIPELINED = 1 } mg_verify_mode;
+ *                        resolved with mg_verify_window.
+ *   MG_VERIFY_FUSED      the synchronous semantics (same committed tokens,
+ *                        kinds and step) at the pipelined cost: every
+ *                        protected row's verifier token for the CURRENT step
+ *                        is computed speculatively inside the step's own
+ *                        weight pass (catch-up tokens as extra GEMM columns),
+ *                        and the gate prot && g < tau only selects whose
+ *                        verifier token is used.  r_verify counts the gated
+ *                        rows as before; verifier_launches / catchup_tokens
+ *                        count the speculative work (every protected row). */
+typedef enum { MG_VERIFY_SYNC = 0, MG_VERIFY_PIPELINED = 1, MG_VERIFY_FUSED = 2 } mg_verify_mode;
 
 /* Sizes the four buffers for `cfg`.  MG_ERR_INVALID on unsupported shapes
  * (d_model % 64, d_ff % 64, (H+2KV)*hd % 128, vocab % 128, head_dim in

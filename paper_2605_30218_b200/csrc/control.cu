@@ -135,6 +135,8 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
     if (a.pend) {  // pipelined verification: the tentative token sits at position p (= pos - 1 here)
       tr = a.pend[slot] != 0;
       p -= 1;
+    } else if (a.list_protected) {  // fused verification: every protected row, before its margin exists
+      tr = a.prot ? a.prot[b] != 0 : true;
     } else {
       const bool prot = a.prot ? a.prot[b] != 0 : true;
       tr = prot && (a.g[b] < a.tau);  // strict <
@@ -247,7 +249,8 @@ __global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
   const int b = blockIdx.x;
   const int slot = a.slots[b];
   const int p = a.pos[slot];
-  const bool tr = a.gate_ran && a.trig[b];
+  const bool listed = a.gate_ran && a.trig[b];
+  const bool tr = listed && (!a.spec || a.g[b] < a.spec_tau);  // fused mode: the gate, strict <
   const int f = a.f_tok[b];
   const int v = tr ? a.v_tok[a.rank[b]] : -1;
   const int kind = !tr ? 0 : (v == f ? 1 : 2);
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
     if (a.margin_out) a.margin_out[b] = a.g[b];
     a.hist[(size_t)slot * a.hist_stride + p + 1] = out;
     a.pos[slot] = p + 1;
-    if (tr) a.shadow_len[slot] = p + 1;
+    if (listed) a.shadow_len[slot] = p + 1;
     if (a.dbg_vtok) {
       a.dbg_vtok[b] = v;
       a.dbg_vg[b] = tr ? a.v_g[a.rank[b]] : 0.f;

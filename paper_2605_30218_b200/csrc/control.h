@@ -28,6 +28,9 @@ struct GateArgs {
   // sits at position pos - 1) instead of prot && g < tau
   const uint8_t* pend;     // [max_slots] or nullptr
   int32_t* rank_slot;      // [max_slots] rank of each listed slot (nullable)
+  // fused same-step verification (MG_VERIFY_FUSED): list every protected row
+  // (p = pos) before the fast forward, independent of the margin
+  int32_t list_protected;
 };
 cudaError_t launch_gate(const GateArgs& a, cudaStream_t st);
 
@@ -57,6 +60,11 @@ struct CommitArgs {
   int hist_stride;
   ColCopy copy;            // shadow -> fast
   int repair_copy;         // 1: copy the verifier column on a repair; 0: token-only
+  // MG_VERIFY_FUSED: trig[b] marks the rows whose verifier ran speculatively
+  // (every protected row); the gate prot && g < spec_tau decides which of them
+  // commit the verifier's result; all of them have their shadow cache caught up
+  int spec;
+  float spec_tau;
   int32_t* tokens_out;
   uint8_t* kind_out;
   float* margin_out;

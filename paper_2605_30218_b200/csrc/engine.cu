@@ -957,6 +957,149 @@ static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const 
   return MG_OK;
 }
 
+// Same-step fused verification (MG_VERIFY_FUSED): every protected row's
+// verifier token for THIS step is computed speculatively in the fast step's own
+// weight pass (its catch-up tokens are extra GEMM columns, its attention runs on
+// the shadow cache with the pinned splits); the gate prot && g < tau then
+// decides, per row, whether the verifier's token is committed (verified /
+// repair) exactly as in MG_VERIFY_SYNC.  Same committed tokens and kinds as the
+// synchronous mode; the host never waits on the device inside a step.
+static mg_status decode_fused(mg_ctx* c, const int32_t* slots, int B, const uint8_t* prot, float tau,
+                              int32_t* tokens_out, uint8_t* kind_out, float* margin_out) {
+  const int S = c->cfg.max_slots;
+  std::vector<char> seen(S, 0);
+  int max_ctx = 1, need_pages = 0;
+  bool any_prot = false;
+  for (int b = 0; b < B; ++b) {
+    const int s = slots[b];
+    if (s < 0 || s >= S || !c->active[s] || seen[s]) return fail(c, MG_ERR_INVALID, "inactive or duplicate slot");
+    seen[s] = 1;
+    const int p = c->pos_h[s];
+    if (p >= c->cfg.max_seq) return fail(c, MG_ERR_CAPACITY, "max_seq reached");
+    if (p / c->PS >= (int)c->pages[s].size()) ++need_pages;
+    if (p + 1 > max_ctx) max_ctx = p + 1;
+    if (!prot || prot[b]) any_prot = true;
+  }
+  if ((int)c->free_pages.size() < need_pages) return fail(c, MG_ERR_CAPACITY, "KV pages exhausted");
+  const bool gate = any_prot && tau > 0.f;
+  // the verifier list (host mirrors are exact in this mode): protected rows in
+  // ascending order, catch-up positions shadow_len .. p
+  std::vector<int> last;
+  int M = 0, vmax = 1;
+  if (gate)
+    for (int b = 0; b < B; ++b) {
+      if (prot && !prot[b]) continue;
+      const int s = slots[b];
+      M += c->pos_h[s] - c->shadow_h[s] + 1;
+      last.push_back(M - 1);
+      if (c->pos_h[s] + 1 > vmax) vmax = c->pos_h[s] + 1;
+    }
+  const int n_list = (int)last.size();
+  size_t ev0 = 0;
+  if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
+  std::vector<std::pair<int, int>> upd;
+  for (int b = 0; b < B; ++b) {
+    const int s = slots[b];
+    if (c->pos_h[s] / c->PS >= (int)c->pages[s].size()) alloc_page(c, s, &upd);
+  }
+  mg_status r;
+  {
+    const int pw = (B + 3) / 4;
+    std::vector<int32_t> w(B + pw + 2 * upd.size());
+    memcpy(w.data(), slots, B * 4);
+    std::vector<uint8_t> pb(pw * 4, 1);
+    if (prot) memcpy(pb.data(), prot, B);
+    memcpy(w.data() + B, pb.data(), pw * 4);
+    for (size_t i = 0; i < upd.size(); ++i) {
+      w[B + pw + 2 * i] = upd[i].first;
+      w[B + pw + 2 * i + 1] = upd[i].second;
+    }
+    if ((r = upload(c, w))) return r;
+    CK(cudaMemcpyAsync(c->slots_d, c->staging_d, B * 4, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(c->prot_d, c->staging_d + B, B, cudaMemcpyDeviceToDevice, c->st));
+    if (!upd.empty()) {
+      k_apply_pt<<<cdiv((int)upd.size(), 128), 128, 0, c->st>>>(c->pt_d, c->staging_d + B + pw, (int)upd.size());
+      CK(cudaGetLastError());
+      c->launches++;
+    }
+  }
+  GateArgs ga{};
+  ga.g = c->f_g; ga.prot = c->prot_d; ga.tau = tau; ga.slots = c->slots_d; ga.B = B;
+  ga.pos = c->pos_d; ga.shadow_len = c->shadow_d; ga.hist = c->hist_d; ga.hist_stride = c->cfg.max_seq + 1;
+  ga.trig = c->trig_d; ga.rank = c->rank_d; ga.ctrl = c->ctrl_d; ga.last = c->last_d;
+  ga.cu_slot = c->cu_slot; ga.cu_pos = c->cu_pos; ga.cu_tok = c->cu_tok; ga.cu_nk = c->cu_nk;
+  ga.list_protected = 1;
+  int Mx = gate ? M : 0;
+  if (gate) {
+    CK(launch_gate(ga, c->st));  // the verifier list, before the forward
+    c->launches++;
+    if (B + M > c->Tmax) {        // too long to ride along: the verifier runs on its own first
+      if ((r = run_det(c, M, last, vmax))) return r;
+      Mx = 0;
+    }
+  }
+  int Mb = Mx, n_lm = Mx > 0 ? n_list : 0;
+  if (Mx > 0) {  // power-of-two buckets (padding repeats real entries): few distinct graphs
+    Mb = 1;
+    while (Mb < Mx) Mb <<= 1;
+    if (B + Mb > c->Tmax) Mb = Mx;
+    int nb = 1;
+    while (nb < n_lm) nb <<= 1;
+    n_lm = nb < B ? nb : B;
+  }
+  Mx = Mb;
+  Sched fs = sched_fast(c, B, max_ctx);
+  Sched ds = sched_det(c, Mx > 0 ? Mx : 1, vmax);
+  r = graphed(c, std::make_tuple(4, B, Mx, n_lm, fs.attn_ns * 65536 + ds.attn_ns, fs.attn_sk), [&]() -> mg_status {
+    CK(launch_prepare_mixed(c->slots_d, B, c->pos_d, c->hist_d, c->cfg.max_seq + 1, c->cu_slot, c->cu_pos, c->cu_tok,
+                            c->cu_nk, Mx, c->ctrl_d, c->mx_slot, c->mx_pos, c->mx_tok, c->mx_nk, c->st));
+    c->launches++;
+    mg_status rr = forward_mixed(c, B, Mx, fs, ds);
+    if (rr) return rr;
+    CK(launch_lm_rows(c->xn, B, c->last_d, c->ctrl_d, n_lm, c->d, c->xlm, c->st));
+    c->launches++;
+    const int T = B + n_lm;
+    if ((rr = gemm(c, c->xlm, 2 * c->cfg.max_batch, T, c->lm, op_lm(c->V, c->d, T, true), c->logits))) return rr;
+    CK(launch_top2(c->logits, B, c->V, c->top2_part, c->nb_top2, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g,
+                   c->nan_d, c->st));
+    c->launches += 2;
+    if (n_lm > 0) {
+      CK(launch_top2(c->logits + (size_t)B * c->V, n_lm, c->V, c->top2_part + (size_t)B * c->nb_top2 * 4,
+                     c->nb_top2, c->v_v1, c->v_tok, c->v_v2, c->v_i2, c->v_g, c->nan_d, c->st));
+      c->launches += 2;
+    }
+    return MG_OK;
+  });
+  if (r) return r;
+  if (c->capture) CK(cudaMemcpyAsync(c->capture, c->logits, (size_t)B * c->V * 4, cudaMemcpyDeviceToDevice, c->st));
+  if (c->capture_v && n_lm > 0)
+    CK(cudaMemcpyAsync(c->capture_v, c->logits + (size_t)B * c->V, (size_t)n_list * c->V * 4,
+                       cudaMemcpyDeviceToDevice, c->st));
+  CommitArgs ca{};
+  ca.B = B; ca.slots = c->slots_d; ca.prot = c->prot_d; ca.gate_ran = gate ? 1 : 0; ca.trig = c->trig_d;
+  ca.rank = c->rank_d; ca.ctrl = c->ctrl_d; ca.f_tok = c->f_tok; ca.g = c->f_g; ca.v_tok = c->v_tok; ca.v_g = c->v_g;
+  ca.pos = c->pos_d; ca.shadow_len = c->shadow_d; ca.hist = c->hist_d; ca.hist_stride = c->cfg.max_seq + 1;
+  ca.copy = col_copy(c, true);
+  ca.repair_copy = c->repair_mode == MG_REPAIR_COLUMN ? 1 : 0;
+  ca.spec = 1; ca.spec_tau = tau;
+  ca.tokens_out = tokens_out; ca.kind_out = kind_out; ca.margin_out = margin_out; ca.stats = c->stats_d;
+  ca.dbg_vtok = c->dbg_vtok; ca.dbg_vg = c->dbg_vg; ca.dbg_kind = c->dbg_kind; ca.dbg_trig = c->dbg_trig;
+  ca.dbg_out = c->dbg_out;
+  CK(launch_commit(ca, c->st));
+  c->launches++;
+  if (c->timing.on) {
+    cudaEventRecord(tevent(c), c->st);
+    c->timing.rec.emplace_back(ev0, c->timing.used - 1, 2, 0.0);
+  }
+  for (int b = 0; b < B; ++b) {
+    const int s = slots[b];
+    c->pos_h[s] += 1;
+    if (gate && (!prot || prot[b])) c->shadow_h[s] = c->pos_h[s];
+  }
+  c->last_B = B;
+  return MG_OK;
+}
+
 static std::string g_init_err;
 
 extern "C" {
@@ -1102,6 +1245,7 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
   if (std::isnan(tau) || tau < 0.f) return fail(c, MG_ERR_INVALID, "threshold must be >= 0");
   if (c->verify_mode == MG_VERIFY_PIPELINED)
     return decode_pipelined(c, slots, B, prot, tau, tokens_out, kind_out, margin_out);
+  if (c->verify_mode == MG_VERIFY_FUSED) return decode_fused(c, slots, B, prot, tau, tokens_out, kind_out, margin_out);
   std::vector<char> seen(c->cfg.max_slots, 0);
   int max_ctx = 1;
   int need_pages = 0;
@@ -1228,7 +1372,7 @@ mg_status mg_set_policy(mg_ctx* c, int32_t fast_schedule, int32_t repair_action,
     return fail(c, MG_ERR_INVALID, "unknown fast schedule");
   if (repair_action != MG_REPAIR_COLUMN && repair_action != MG_REPAIR_TOKEN_ONLY)
     return fail(c, MG_ERR_INVALID, "unknown repair action");
-  if (verify_mode != MG_VERIFY_SYNC && verify_mode != MG_VERIFY_PIPELINED)
+  if (verify_mode != MG_VERIFY_SYNC && verify_mode != MG_VERIFY_PIPELINED && verify_mode != MG_VERIFY_FUSED)
     return fail(c, MG_ERR_INVALID, "unknown verify mode");
   mg_status r = pipe_refresh(c);
   if (r) return r;
