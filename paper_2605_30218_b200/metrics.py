@@ -98,3 +98,26 @@ def rates(stats: dict) -> dict:
         "r_verify": stats["triggers"] / p if p else 0.0,
         "r_repair": stats["repairs"] / p if p else 0.0,
     }
+
+
+def kv_deviation(batched_cols, ref_cols):
+    """S2.2 Observation 2: E^K_p = ||K^{bs=N}_{:,p,:} - K^{ref}_{:,p,:}||_2
+    and E^V_p likewise, per layer and position.  Inputs: per position p a
+    bf16 column [L][2 (K, V)][KV][hd] (uint16 bit patterns, as
+    mgd_read_column returns them).  Returns (EK, EV) float64 arrays [P][L]."""
+    import numpy as np
+    a = np.asarray(batched_cols, dtype=np.uint16).astype(np.uint32) << 16
+    b = np.asarray(ref_cols, dtype=np.uint16).astype(np.uint32) << 16
+    d = a.view(np.float32).astype(np.float64) - b.view(np.float32).astype(np.float64)
+    e = np.sqrt((d * d).sum(axis=(-2, -1)))        # [P][L][2]
+    return e[..., 0], e[..., 1]
+
+
+def divergence_aligned(err, p0: int, p_div):
+    """Fig. fig:err_vs_dist: per offset Delta = p - p_div the
+    deviation; positions are p0 + index.  Without a divergence, Delta is None."""
+    out = {}
+    for i, row in enumerate(err):
+        delta = None if p_div is None else p0 + i - p_div
+        out.setdefault(delta, []).append(row)
+    return out

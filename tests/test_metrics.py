@@ -66,3 +66,26 @@ def test_seq_determinism_and_rates():
     assert metrics.seq_determinism([[1, 2], [1, 3]], [[1, 2], [1, 2]]) == 0.5
     r = metrics.rates({"triggers": 10, "repairs": 2, "protected_rows": 40})
     assert r == {"r_verify": 0.25, "r_repair": 0.05}
+
+
+def test_kv_deviation_closed_form():
+    """E^K_p / E^V_p: identical columns give 0; one element off
+    by a known bf16 difference gives exactly that L2 norm, in its own layer,
+    position and K/V slot only; sqrt of a sum over heads and dims."""
+    import numpy as np
+    L, KV, hd, P = 3, 2, 4, 5
+    rng = np.random.default_rng(0)
+    base = (rng.integers(0x3F00, 0x4000, size=(P, L, 2, KV, hd))).astype(np.uint16)
+    ek, ev = metrics.kv_deviation(base, base)
+    assert ek.shape == (P, L) and not ek.any() and not ev.any()
+    other = base.copy()
+    other[2, 1, 1, 0, 3] = 0x3F80            # 1.0
+    other[2, 1, 1, 1, 0] = 0x4000            # 2.0
+    a = base.astype(np.uint32) << 16
+    x = a.view(np.float32).astype(np.float64)
+    want = np.sqrt((x[2, 1, 1, 0, 3] - 1.0) ** 2 + (x[2, 1, 1, 1, 0] - 2.0) ** 2)
+    ek, ev = metrics.kv_deviation(base, other)
+    assert not ek.any()
+    assert ev[2, 1] == pytest.approx(want, rel=1e-12) and np.count_nonzero(ev) == 1
+    al = metrics.divergence_aligned(ev, 10, 12)
+    assert sorted(al) == [-2, -1, 0, 1, 2] and al[0][0][1] == ev[2, 1]
