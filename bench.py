@@ -800,7 +800,7 @@ def kv_trace(eng, shp, B, P, steps, trials):
         eng.release(0)
         d = metrics.first_divergence(seq, ref)
         ek, ev = metrics.kv_deviation(fast, shadow)
-        p_div = None if d is None else P + d - 1   # the first column whose input token differs
+        p_div = None if d is None else P + d       # the first column whose input token differs (token d sits at P + d)
         if p_div is not None:
             n_div += 1
         for i in range(steps):

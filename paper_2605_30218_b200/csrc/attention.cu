@@ -101,6 +101,12 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
   const int t = blockIdx.x, kvh = blockIdx.y, sp = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.H, G = a.H / a.KV;
+  // token group: the second one (t >= T1) is the verifier's in a mixed launch
+  const bool g1 = a.T1 > 0 && t >= a.T1;
+  const CacheView& cview = g1 ? a.cache1 : a.cache;
+  const CUtensorMap* kmp = g1 ? &a.kvmap1 : &a.kmap;
+  const CUtensorMap* vmp = g1 ? &a.kvmap1 : &a.vmap;
+  const int split_keys = g1 ? a.split_keys1 : a.split_keys;
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NBAR; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
@@ -108,12 +114,12 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
   __syncthreads();
   if (!a.prewait) griddep();
   const int n = a.n_keys[t];
-  const int lo = sp * a.split_keys;
+  const int lo = sp * split_keys;
   if (lo >= n) return;
-  const int hi = min(n, lo + a.split_keys);
+  const int hi = min(n, lo + split_keys);
   const int nblk = (hi - lo + 15) >> 4;
   const int nbw = nblk > warp ? (nblk - warp + 3) >> 2 : 0;  // blocks of this warp
-  const int n_sp = (n + a.split_keys - 1) / a.split_keys;
+  const int n_sp = (n + split_keys - 1) / split_keys;
   uint8_t* kring = sm + C::RING_OFF + warp * C::WRING;
   uint8_t* vring = kring + RK * C::BLK;
   uint64_t* kfull = bars + 1 + warp * (RK + RV);
@@ -128,7 +134,7 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
     if (i < nbw) {
       const int key0 = lo + 16 * (warp + 4 * i);
       if (a.paged) {
-        const CacheView& cv = a.cache;
+        const CacheView& cv = cview;
         const int page = cv.pt[(size_t)a.slot[t] * cv.max_pages + key0 / cv.page_size];
         o_sl = (cv.layer * cv.n_pages + page) * 2 * a.KV + kvh;
         o_row = key0 % cv.page_size;
@@ -146,7 +152,7 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
       mbar_expect_tx(&kfull[s], C::BLK);
 #pragma unroll
       for (int h = 0; h < C::HALVES; ++h)
-        tma_load_3d(kring + s * C::BLK + h * 2048, &a.kmap, &kfull[s], 64 * h, row, sl);
+        tma_load_3d(kring + s * C::BLK + h * 2048, kmp, &kfull[s], 64 * h, row, sl);
     }
   };
   auto issue_v = [&](int i) {
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
       mbar_expect_tx(&vfull[s], C::BLK);
 #pragma unroll
       for (int h = 0; h < C::HALVES; ++h)
-        tma_load_3d(vring + s * C::BLK + h * 2048, &a.vmap, &vfull[s], 64 * h, row, sl + vsl);
+        tma_load_3d(vring + s * C::BLK + h * 2048, vmp, &vfull[s], 64 * h, row, sl + vsl);
     }
   };
   coords(0, k_sl, k_row);
@@ -219,7 +225,7 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
       } else {
         kvn[g * HD + i] = oa;
         kvn[g * HD + i + h2] = ob;
-        uint16_t* dst = cache_ptr(a.cache, a.slot[t], p, g, kvh);
+        uint16_t* dst = cache_ptr(cview, a.slot[t], p, g, kvh);
         dst[i] = oa;
         dst[i + h2] = ob;
       }
@@ -445,6 +451,7 @@ static int g_attn_ring = 0;
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st) {
   if (a.H % a.KV || a.H / a.KV > 16 || !a.counter || a.split_keys < 64 || a.split_keys % 64 || a.n_splits < 1)
     return cudaErrorInvalidValue;
+  if (a.T1 > 0 && a.T1 < a.T && (a.split_keys1 < 64 || a.split_keys1 % 64)) return cudaErrorInvalidValue;
   if (!g_attn_ring) {
     const char* s = getenv("MG_ATTN_RING");
     const int v = s ? atoi(s) : 0;

@@ -262,6 +262,9 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   size_t attn_rows_fast = (size_t)g.max_batch * c->H * cdiv(g.max_seq, 64);
   size_t attn_rows_det = (size_t)c->Tv * c->H * cdiv(g.max_seq, c->det_sk);
   size_t attn_rows = attn_rows_fast > attn_rows_det ? attn_rows_fast : attn_rows_det;
+  // mixed fast + verifier launches (forward_mixed): up to Tmax tokens, splits >= 64 keys
+  const size_t attn_rows_mixed = (size_t)(g.max_batch > c->Tv ? g.max_batch : c->Tv) * c->H * cdiv(g.max_seq, 64);
+  if (attn_rows_mixed > attn_rows) attn_rows = attn_rows_mixed;
 
   Carver s(ws);
   const int Tm = c->Tmax, B = g.max_batch;
@@ -450,7 +453,7 @@ static mg_status forward(mg_ctx* c, int T, const int32_t* slot, const int32_t* p
 // runs on the B+M columns (a column's result does not depend on the others,
 // DESIGN.md 7.2), attention is launched once per row group with its own cache
 // and split schedule.
-static mg_status forward_mixed(mg_ctx* c, int B, int M, const Sched& fs, const Sched& ds) {
+static mg_status forward_mixed(mg_ctx* c, int B, int M, const Sched& fs, const Sched& ds, bool unified) {
   const int T = B + M, Tm = c->Tmax;
   const float eps = c->cfg.rms_eps;
   const OpSched oq = op_det(c->NQKV, c->d, T), oo = op_det(c->d, c->NQ, T), ogu = op_det(2 * c->F, c->d, T),
@@ -462,7 +465,10 @@ static mg_status forward_mixed(mg_ctx* c, int B, int M, const Sched& fs, const S
     const LayerW& w = c->layers[l];
     mg_status r = gemm(c, c->xn, Tm, T, w.qkv, oq, c->part);
     if (r) return r;
-    // fast rows: QKV epilogue fused into attention, fast cache, batch-shaped splits
+    // fast rows: QKV epilogue fused into attention, fast cache, batch-shaped splits.
+    // unified: every verifier token appends exactly one column of its own row
+    // (gap 1), so it takes the same fused form in the SAME launch, as a second
+    // token group on the shadow cache with the pinned splits
     CacheView cf = cache_view(c, 0, l);
     AttnArgs aa{};
     aa.q = c->q; aa.cache = cf; aa.paged = 1; aa.slot = c->mx_slot; aa.n_keys = c->mx_nk;
@@ -472,9 +478,14 @@ static mg_status forward_mixed(mg_ctx* c, int B, int M, const Sched& fs, const S
     aa.prewait = 1; aa.fuse_qkv = 1;
     aa.qkv_part = c->part; aa.qkv_ps = oq.ps(); aa.bias = w.bqkv; aa.pos = c->mx_pos;
     aa.rcos = c->rope_cos; aa.rsin = c->rope_sin; aa.part_T = T;
+    if (unified && M > 0) {
+      aa.T = T; aa.T1 = B;
+      aa.cache1 = cache_view(c, 1, l); aa.kvmap1 = c->kv_map[1]; aa.split_keys1 = ds.attn_sk;
+      aa.n_splits = fs.attn_ns > ds.attn_ns ? fs.attn_ns : ds.attn_ns;
+    }
     CK(launch_attention(aa, c->st));
     c->launches++;
-    if (M > 0) {
+    if (M > 0 && !unified) {
       // verifier rows: separate epilogue into the shadow cache, pinned splits
       CacheView cs = cache_view(c, 1, l);
       CK(launch_epi_qkv(c->part + (size_t)B * c->NQKV, oq.ps(), w.bqkv, c->mx_pos + B, M, c->H, c->KV, c->hd,
@@ -888,14 +899,16 @@ static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const 
     while (nb < n_lm) nb <<= 1;
     n_lm = nb < B ? nb : B;
   }
+  const bool unified = Mx > 0 && M == n_pend;  // every pending row catches up one token: one attention launch
   Mx = Mb;
   Sched fs = sched_fast(c, B, max_ctx);
   Sched ds = sched_det(c, Mx > 0 ? Mx : 1, vmax);
-  r = graphed(c, std::make_tuple(3, B, Mx, n_lm, fs.attn_ns * 65536 + ds.attn_ns, fs.attn_sk), [&]() -> mg_status {
+  r = graphed(c, std::make_tuple(3, B, Mx, n_lm, fs.attn_ns * 65536 + ds.attn_ns * 2 + (unified ? 1 : 0), fs.attn_sk),
+              [&]() -> mg_status {
     CK(launch_prepare_mixed(c->slots_d, B, c->pos_d, c->hist_d, c->cfg.max_seq + 1, c->cu_slot, c->cu_pos, c->cu_tok,
                             c->cu_nk, Mx, c->ctrl_d, c->mx_slot, c->mx_pos, c->mx_tok, c->mx_nk, c->st));
     c->launches++;
-    mg_status rr = forward_mixed(c, B, Mx, fs, ds);
+    mg_status rr = forward_mixed(c, B, Mx, fs, ds, unified);
     if (rr) return rr;
     CK(launch_lm_rows(c->xn, B, c->last_d, c->ctrl_d, n_lm, c->d, c->xlm, c->st));
     c->launches++;
@@ -1047,14 +1060,16 @@ static mg_status decode_fused(mg_ctx* c, const int32_t* slots, int B, const uint
     while (nb < n_lm) nb <<= 1;
     n_lm = nb < B ? nb : B;
   }
+  const bool unified = Mx > 0 && M == n_list;  // every protected row catches up one token: one attention launch
   Mx = Mb;
   Sched fs = sched_fast(c, B, max_ctx);
   Sched ds = sched_det(c, Mx > 0 ? Mx : 1, vmax);
-  r = graphed(c, std::make_tuple(4, B, Mx, n_lm, fs.attn_ns * 65536 + ds.attn_ns, fs.attn_sk), [&]() -> mg_status {
+  r = graphed(c, std::make_tuple(4, B, Mx, n_lm, fs.attn_ns * 65536 + ds.attn_ns * 2 + (unified ? 1 : 0), fs.attn_sk),
+              [&]() -> mg_status {
     CK(launch_prepare_mixed(c->slots_d, B, c->pos_d, c->hist_d, c->cfg.max_seq + 1, c->cu_slot, c->cu_pos, c->cu_tok,
                             c->cu_nk, Mx, c->ctrl_d, c->mx_slot, c->mx_pos, c->mx_tok, c->mx_nk, c->st));
     c->launches++;
-    mg_status rr = forward_mixed(c, B, Mx, fs, ds);
+    mg_status rr = forward_mixed(c, B, Mx, fs, ds, unified);
     if (rr) return rr;
     CK(launch_lm_rows(c->xn, B, c->last_d, c->ctrl_d, n_lm, c->d, c->xlm, c->st));
     c->launches++;

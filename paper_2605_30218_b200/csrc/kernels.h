@@ -142,6 +142,12 @@ struct AttnArgs {
   // offset of this launch's token 0 in the Q tensor map
   int32_t part_T;
   int32_t q_row0;
+  // second token group (mixed fast + verifier launch): tokens t >= T1 read and
+  // append through cache1 / kvmap1 with split_keys1 (T1 == 0 or >= T: one group)
+  int32_t T1;
+  int32_t split_keys1;
+  CacheView cache1;
+  CUtensorMap kvmap1;
 };
 bool make_tmap_3d(CUtensorMap* m, const void* base, int d0, int64_t d1, int64_t d2, int box1);
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st);

@@ -115,6 +115,8 @@ def test_full_size_sampled_row_parity(orc, name):
         q_tol = max(TOL, 2 * float(np.quantile(noise, 0.999)))
         m_tol = max(1.5 * TOL, 2 * float(noise.max()))
         ef = np.abs(fl[t] - ra["logits"][0])
+        print(f"[fullsize] {name} step {t}: gpu-vs-oracle p99.9 {np.quantile(ef, 0.999):.4f} max {ef.max():.4f}; "
+              f"oracle self-noise p99.9 {np.quantile(noise, 0.999):.4f} max {noise.max():.4f}")
         assert np.quantile(ef, 0.999) <= q_tol, (t, float(np.quantile(ef, 0.999)), q_tol)
         assert ef.max() <= m_tol, (t, float(ef.max()), m_tol)
         if ra["g"][0] > 2 * ef.max():
