@@ -73,6 +73,17 @@ mg_status mgd_top2(const float* logits, int32_t T, int32_t V, float* v1, int32_t
 mg_status mgd_gate(const float* g, const uint8_t* prot, int32_t B, float tau, uint8_t* trig, int32_t* rows,
                    int32_t* count, void* stream);
 
+/* ---- controlled perturbations (SURVEY 8(b) test-only exports) ---- */
+/* SPEC.md:76-84 injected logit noise on the FAST rows' logits (never the
+ * verifier's): l[v] += amp * (u * 2^-23) with u = (splitmix64(seed ^ B<<56 ^
+ * slot<<44 ^ pos<<20 ^ v) >> 40) - 2^23 -- the formula of the oracle's
+ * fast_sched(noise_amp, noise_seed), bit-exact; exactly zero at batch 1.
+ * amp = 0 turns it off.  While on, the step runs without CUDA graphs. */
+mg_status mgd_set_inject(mg_ctx* ctx, float amp, uint64_t seed);
+/* Fast path with the attention split schedule of batch size B_as_if (0: the
+ * real batch) -- controlled batch-shape flips without changing the batch. */
+mg_status mgd_force_schedule(mg_ctx* ctx, int32_t B_as_if);
+
 /* ---- engine introspection (synchronise; host outputs) ---- */
 /* Fast (which=0) or shadow (which=1) column (slot, pos) -> out [L][2][KV][hd] */
 mg_status mgd_read_column(mg_ctx* ctx, int32_t which, int32_t slot, int32_t pos, uint16_t* out_host);

@@ -474,6 +474,34 @@ cudaError_t launch_lm_rows(const uint16_t* src, int B, const int32_t* last, cons
   return launch_k(k_lm_rows, dim3(B + n), dim3(128), 0, st, src, B, last, ctrl, d, dst);
 }
 
+// ------------------------------------------------------------------ test-only perturbation
+// SPEC.md:76-84 injected logit noise (mgd_set_inject; never on by default):
+// l[v] += amp * (u * 2^-23), u = (splitmix64(seed ^ B<<56 ^ slot<<44 ^ pos<<20 ^ v) >> 40) - 2^23,
+// exactly zero at batch 1 -- the documented formula the oracle applies too.
+__device__ __forceinline__ uint64_t inj_mix(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void k_inject(float* logits, int B, int V, float amp, unsigned long long seed, const int32_t* slot,
+                         const int32_t* pos) {
+  griddep();
+  const int b = blockIdx.y;
+  const uint64_t key = seed ^ ((uint64_t)B << 56) ^ ((uint64_t)slot[b] << 44) ^ ((uint64_t)pos[b] << 20);
+  float* l = logits + (size_t)b * V;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+    const int u = (int)(inj_mix(key ^ (uint64_t)v) >> 40) - 8388608;
+    l[v] = __fadd_rn(l[v], __fmul_rn(amp, __fmul_rn((float)u, 1.1920928955078125e-07f)));
+  }
+}
+
+cudaError_t launch_inject(float* logits, int B, int V, float amp, unsigned long long seed, const int32_t* slot,
+                          const int32_t* pos, cudaStream_t st) {
+  if (B <= 1 || !(amp > 0.f)) return cudaSuccess;
+  return launch_k(k_inject, dim3(16, B), dim3(256), 0, st, logits, B, V, amp, seed, slot, pos);
+}
+
 // prefill bookkeeping: hist[slot][len] = token, pos = shadow_len = len
 __global__ void k_prefill_done(int32_t* hist, int hist_stride, int32_t* pos, int32_t* shadow_len, int slot, int len,
                                const int32_t* tok) {

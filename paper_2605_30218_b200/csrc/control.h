@@ -141,6 +141,10 @@ cudaError_t launch_prepare_mixed(const int32_t* slots, int B, const int32_t* pos
 cudaError_t launch_lm_rows(const uint16_t* src, int B, const int32_t* last, const int32_t* ctrl, int n, int d,
                            uint16_t* dst, cudaStream_t st);
 
+// test-only SPEC.md:76-84 logit perturbation of the fast rows (mgd_set_inject)
+cudaError_t launch_inject(float* logits, int B, int V, float amp, unsigned long long seed, const int32_t* slot,
+                          const int32_t* pos, cudaStream_t st);
+
 cudaError_t launch_prepare(const int32_t* slots, int B, const int32_t* pos, const int32_t* hist, int hist_stride,
                            int32_t* f_slot, int32_t* f_pos, int32_t* f_tok, int32_t* f_nk, cudaStream_t st);
 cudaError_t launch_prefill_done(int32_t* hist, int hist_stride, int32_t* pos, int32_t* shadow_len, int slot, int len,

@@ -172,7 +172,7 @@ static Sched sched_fast(const mg_ctx* c, int T, int max_ctx) {
   // token's last key exit at once).
   (void)max_ctx;
   const int cap = c->cfg.max_seq;
-  const int ctas = T * c->KV, target = 2 * kSMs;
+  const int ctas = (c->force_B > 0 ? c->force_B : T) * c->KV, target = 2 * kSMs;  // force_B: test-only
   int ns = 1;
   if (ctas < target) ns = clampi(cdiv(target, ctas), 1, cdiv(cap, 128) > 1 ? cdiv(cap, 128) : 1);
   s.attn_sk = cdiv(cdiv(cap, ns), 64) * 64;
@@ -617,9 +617,14 @@ static mg_status forward_chain(mg_ctx* c, int T, const int32_t* slot, const int3
 
 // LM head + top-2 over the final-normed rows xnorm[0..T)
 static mg_status lm_head(mg_ctx* c, const uint16_t* xnorm, int xrows, int T, const OpSched& o, float* v1,
-                         int32_t* i1, float* v2, int32_t* i2, float* g) {
+                         int32_t* i1, float* v2, int32_t* i2, float* g, const int32_t* inj_slot = nullptr,
+                         const int32_t* inj_pos = nullptr) {
   mg_status r = gemm(c, xnorm, xrows, T, c->lm, o, c->logits);
   if (r) return r;
+  if (inj_slot && c->inj_amp > 0.f) {  // test-only SPEC.md:76-84 perturbation of the fast rows
+    CK(launch_inject(c->logits, T, c->V, c->inj_amp, c->inj_seed, inj_slot, inj_pos, c->st));
+    c->launches++;
+  }
   CK(launch_top2(c->logits, T, c->V, c->top2_part, c->nb_top2, v1, i1, v2, i2, g, c->nan_d, c->st));
   c->launches += 2;
   return MG_OK;
@@ -675,7 +680,7 @@ static mg_status apply_pt(mg_ctx* c, const std::vector<std::pair<int, int>>& upd
 // the second, replayed afterwards (PDL edges are kept as programmatic edges).
 template <class F>
 static mg_status graphed(mg_ctx* c, const std::tuple<int, int, int, int, int, int>& key, F&& body) {
-  if (!c->use_graphs || c->timing.on || c->capture || c->capture_v) return body();
+  if (!c->use_graphs || c->timing.on || c->capture || c->capture_v || c->inj_amp > 0.f) return body();
   auto& g = c->graphs[key];
   if (g.exec) {
     CK(cudaGraphLaunch(g.exec, c->st));
@@ -914,6 +919,10 @@ static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const 
     c->launches++;
     const int T = B + n_lm;
     if ((rr = gemm(c, c->xlm, 2 * c->cfg.max_batch, T, c->lm, op_lm(c->V, c->d, T, true), c->logits))) return rr;
+    if (c->inj_amp > 0.f) {  // test-only perturbation of the fast rows (B of them)
+      CK(launch_inject(c->logits, B, c->V, c->inj_amp, c->inj_seed, c->mx_slot, c->mx_pos, c->st));
+      c->launches++;
+    }
     CK(launch_top2(c->logits, B, c->V, c->top2_part, c->nb_top2, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g,
                    c->nan_d, c->st));
     c->launches += 2;
@@ -1075,6 +1084,10 @@ static mg_status decode_fused(mg_ctx* c, const int32_t* slots, int B, const uint
     c->launches++;
     const int T = B + n_lm;
     if ((rr = gemm(c, c->xlm, 2 * c->cfg.max_batch, T, c->lm, op_lm(c->V, c->d, T, true), c->logits))) return rr;
+    if (c->inj_amp > 0.f) {  // test-only perturbation of the fast rows (B of them)
+      CK(launch_inject(c->logits, B, c->V, c->inj_amp, c->inj_seed, c->mx_slot, c->mx_pos, c->st));
+      c->launches++;
+    }
     CK(launch_top2(c->logits, B, c->V, c->top2_part, c->nb_top2, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g,
                    c->nan_d, c->st));
     c->launches += 2;
@@ -1315,7 +1328,7 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
     c->launches++;
     mg_status rr = forward(c, B, c->f_slot, c->f_pos, c->f_tok, c->f_nk, 0, fs);
     if (rr) return rr;
-    return lm_head(c, c->xn, c->Tmax, B, fs.lm, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g);
+    return lm_head(c, c->xn, c->Tmax, B, fs.lm, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g, c->f_slot, c->f_pos);
   });
   if (r) return r;
   if (c->capture) CK(cudaMemcpyAsync(c->capture, c->logits, (size_t)B * c->V * 4, cudaMemcpyDeviceToDevice, c->st));
@@ -1648,6 +1661,19 @@ mg_status mgd_schedule(mg_ctx* c, int32_t T, int32_t det, int32_t max_ctx, int32
   auto sp = [](const OpSched& x) { return x.G > 0 ? -x.G : x.splits; };  // < 0: stream-K over -v CTAs
   o[0] = sp(s.qkv); o[1] = sp(s.o); o[2] = sp(s.gu); o[3] = sp(s.down); o[4] = sp(s.lm);
   o[5] = -s.attn_sk; o[6] = s.qkv.impl; o[7] = s.qkv.mma_n;
+  return MG_OK;
+}
+
+mg_status mgd_set_inject(mg_ctx* c, float amp, uint64_t seed) {
+  if (!c || std::isnan(amp) || amp < 0.f) return MG_ERR_INVALID;
+  c->inj_amp = amp;
+  c->inj_seed = seed;
+  return MG_OK;
+}
+
+mg_status mgd_force_schedule(mg_ctx* c, int32_t B_as_if) {
+  if (!c || B_as_if < 0 || B_as_if > c->cfg.max_batch * 64) return MG_ERR_INVALID;
+  c->force_B = B_as_if;
   return MG_OK;
 }
 

@@ -92,6 +92,9 @@ struct mg_ctx {
   bool f_sync = false;       // a pipelined step's readback is in flight
   std::vector<char> pend_h;
   int fast_mode = 0;         // mg_fast_schedule (mg_set_policy)
+  float inj_amp = 0.f;       // test-only logit perturbation (mgd_set_inject)
+  unsigned long long inj_seed = 0;
+  int force_B = 0;           // test-only: fast attention splits of another batch size (mgd_force_schedule)
   int repair_mode = 0;       // mg_repair_action
   int det_sk = 512;          // verifier attention keys per split (A14; MG_DET_SK for measurement)  // chain L2 run-ahead (k-blocks per CTA; measured harmful, off)
   CUtensorMap attn_qmap, kv_map[2];      // TMA maps: q [Tmax][H][hd]; pools (fast, shadow)

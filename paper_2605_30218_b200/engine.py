@@ -142,6 +142,14 @@ class Engine:
               self.ctx, "mgd_last_step")
         return r
 
+    def set_inject(self, amp: float, seed: int = 0):
+        """Test-only SPEC.md:76-84 logit noise on the fast rows (mg_debug.h)."""
+        check(lib().mgd_set_inject(self.ctx, float(amp), int(seed)), self.ctx, "mgd_set_inject")
+
+    def force_schedule(self, B_as_if: int):
+        """Test-only: fast attention splits of batch size B_as_if (0: off)."""
+        check(lib().mgd_force_schedule(self.ctx, int(B_as_if)), self.ctx, "mgd_force_schedule")
+
     def capture_logits(self, buf):
         check(lib().mgd_capture_logits(self.ctx, C.c_void_p(buf.data_ptr()) if buf is not None else None),
               self.ctx, "capture")

@@ -318,3 +318,78 @@ def test_fused_equals_sync(torch, tiny, tau, prot_mode, vc):
     assert runs[0][0] == runs[1][0]
     assert np.array_equal(runs[0][1], runs[1][1])
     assert runs[0][2] == runs[1][2]
+
+
+def test_injected_noise_matches_oracle(orc, torch, tiny):
+    """mgd_set_inject (SURVEY 8(b) test-only export): the GPU adds
+    the oracle's documented perturbation bit for bit, so with real forced
+    flips the GPU's per-step margins, fast tokens and gate decisions replay
+    through the oracle (teacher-forced on the GPU's committed tokens and kinds)
+    within the logit tolerance; repairs fire; at batch 1 the noise is zero."""
+    shp, m = tiny
+    B, steps, amp, seed, tau = 4, 12, 0.5, 9, 0.3
+    prompts = inputs.prompts(B, inputs.ragged_lengths(B, 8, 20, seed=8), shp["vocab"], seed=370)
+    prot = inputs.protected_mask(B, "all")
+    eng = _engine(shp, B)
+    eng.set_inject(amp, seed)
+    first = [eng.prefill(i, p) for i, p in enumerate(prompts)]
+    out = torch.empty(B, dtype=torch.int32, device="cuda")
+    kind = torch.empty(B, dtype=torch.uint8, device="cuda")
+    det = orc.det_sched()
+    st = orc.State(m, B, 64)
+    if [st.prefill(i, p, det) for i, p in enumerate(prompts)] != first:
+        pytest.skip("prefill token inside the ambiguity band")
+    fs = orc.fast_sched(B, noise_amp=amp, noise_seed=seed)
+    rep = checked = 0
+    for _ in range(steps):
+        eng.step(list(range(B)), prot, tau, out, kind)
+        r = eng.last_step(B)
+        o = out.cpu().numpy()
+        ro = st.step(np.arange(B), prot, tau, fs, det, forced_trig=r["trig"], forced_out=o, forced_kind=r["kind"])
+        for b in range(B):
+            assert abs(float(r["g"][b]) - float(ro["g"][b])) <= BAND, (b, r["g"][b], ro["g"][b])
+            if ro["g"][b] > BAND:
+                assert r["f_tok"][b] == ro["f_tok"][b]
+                checked += 1
+            if abs(float(ro["g"][b]) - tau) > BAND:
+                assert bool(r["trig"][b]) == bool(ro["g"][b] < tau)
+        rep += int((r["kind"] == 2).sum())
+    assert rep > 0 and checked > B * steps // 2
+    eng.close()
+    st.close()
+    # batch 1: the perturbation is exactly zero
+    seqs = []
+    for a in (0.0, amp):
+        e1 = _engine(shp, 1)
+        e1.set_inject(a, seed)
+        seqs.append(_decode(torch, e1, prompts[:1], 10, 0.0)[0])
+        e1.close()
+    assert seqs[0] == seqs[1]
+
+
+def test_force_schedule_reproduces_batch_shape(torch, tiny):
+    """mgd_force_schedule: a row decoded alone with the attention splits of
+    batch 8 gives bit-identical fast logits to the same row inside a batch of
+    8 (the GEMMs are column-invariant), i.e. a controlled batch-shape flip
+    source without changing the batch."""
+    shp, _ = tiny
+    V = shp["vocab"]
+    prompts = inputs.prompts(8, inputs.ragged_lengths(8, 8, 23, seed=51), shp["vocab"], seed=380)
+    caps = []
+    for B, force in ((8, 0), (1, 8)):
+        eng = _engine(shp, B, max_seq=4096)   # capacity large enough that batch 1 and 8 split differently
+        assert eng.schedule(1, False, 4096)["attn_chunk"] != eng.schedule(8, False, 4096)["attn_chunk"]
+        eng.force_schedule(force)
+        cap = torch.empty((B, V), dtype=torch.float32, device="cuda")
+        eng.capture_logits(cap)
+        for i, p in enumerate(prompts[:B]):
+            eng.prefill(i, p)
+        out = torch.empty(B, dtype=torch.int32, device="cuda")
+        lg = []
+        for _ in range(4):
+            eng.step(list(range(B)), None, 0.0, out)
+            lg.append(cap[0].cpu().numpy().copy())
+        caps.append(lg)
+        eng.close()
+    for a, b in zip(*caps):
+        assert np.array_equal(a, b)
