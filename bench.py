@@ -600,8 +600,13 @@ def run_reference(args):
     return {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "tok/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": f"{args.model}-shaped {args.workload} decode",
-                                            "model": args.model, "tau": tau},
+            "data": "synthetic",
+            "config": {"workload": f"{args.model}-shaped {args.workload} decode, batch {args.batch}/GPU, "
+                                   f"protected={args.protected}, tau={tau}",
+                       "model": args.model, "global_batch": args.batch, "parallelism": "dp1 (rank 0 only)",
+                       "tau": tau, "protected": args.protected,
+                       "sample": f"one row of the {args.batch}-row batch per step (the oracle decodes rows "
+                                 "independently; batch-shaped reduction plan of batch 1), 8-token prefill"},
             "cpu_baseline": {"value": round(v, 5), "unit": "tok/s", "cores": cores, "kind": "oracle",
                              "sample": "one row of the batch per step (batch 1), 8-token prefill"},
             "e2e": {"value": round(v, 5), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
