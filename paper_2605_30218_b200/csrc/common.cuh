@@ -59,6 +59,50 @@ __host__ __device__ __forceinline__ int part_count(const PartSpec& p, int n) {
   return streamk_owner((long long)(m + 1) * p.KB - 1, W, p.G) - streamk_owner((long long)m * p.KB, W, p.G) + 1;
 }
 
+// ------------------------------------------------------------------ top-2
+// top-1/top-2 under the total order (value desc, id asc): exact, so any merge
+// order gives the same (v1, i1, v2, i2) (A6)
+struct Top2 {
+  float v1;
+  int i1;
+  float v2;
+  int i2;
+};
+
+MG_DEV bool better(float a, int ia, float b, int ib) { return a > b || (a == b && ia < ib); }
+
+MG_DEV void t2_push(Top2& t, float v, int i) {
+  if (better(v, i, t.v1, t.i1)) {
+    t.v2 = t.v1;
+    t.i2 = t.i1;
+    t.v1 = v;
+    t.i1 = i;
+  } else if (better(v, i, t.v2, t.i2)) {
+    t.v2 = v;
+    t.i2 = i;
+  }
+}
+// merge two top-2 sets over disjoint index ranges
+MG_DEV Top2 t2_merge(const Top2& a, const Top2& b) {
+  Top2 r;
+  if (better(a.v1, a.i1, b.v1, b.i1)) {
+    r.v1 = a.v1; r.i1 = a.i1;
+    if (better(a.v2, a.i2, b.v1, b.i1)) { r.v2 = a.v2; r.i2 = a.i2; } else { r.v2 = b.v1; r.i2 = b.i1; }
+  } else {
+    r.v1 = b.v1; r.i1 = b.i1;
+    if (better(a.v1, a.i1, b.v2, b.i2)) { r.v2 = a.v1; r.i2 = a.i1; } else { r.v2 = b.v2; r.i2 = b.i2; }
+  }
+  return r;
+}
+MG_DEV Top2 t2_shfl(const Top2& t, int off) {
+  Top2 o;
+  o.v1 = __shfl_xor_sync(0xffffffffu, t.v1, off);
+  o.i1 = __shfl_xor_sync(0xffffffffu, t.i1, off);
+  o.v2 = __shfl_xor_sync(0xffffffffu, t.v2, off);
+  o.i2 = __shfl_xor_sync(0xffffffffu, t.i2, off);
+  return o;
+}
+
 // ------------------------------------------------------------------ PDL
 // Programmatic dependent launch: every kernel waits for its prerequisite
 // grid before touching data it produced, then lets the next grid launch

@@ -18,47 +18,6 @@
 
 namespace mg {
 
-struct Top2 {
-  float v1;
-  int i1;
-  float v2;
-  int i2;
-};
-
-__device__ __forceinline__ bool better(float a, int ia, float b, int ib) { return a > b || (a == b && ia < ib); }
-
-__device__ __forceinline__ void t2_push(Top2& t, float v, int i) {
-  if (better(v, i, t.v1, t.i1)) {
-    t.v2 = t.v1;
-    t.i2 = t.i1;
-    t.v1 = v;
-    t.i1 = i;
-  } else if (better(v, i, t.v2, t.i2)) {
-    t.v2 = v;
-    t.i2 = i;
-  }
-}
-// merge two top-2 sets over disjoint index ranges
-__device__ __forceinline__ Top2 t2_merge(const Top2& a, const Top2& b) {
-  Top2 r;
-  if (better(a.v1, a.i1, b.v1, b.i1)) {
-    r.v1 = a.v1; r.i1 = a.i1;
-    if (better(a.v2, a.i2, b.v1, b.i1)) { r.v2 = a.v2; r.i2 = a.i2; } else { r.v2 = b.v1; r.i2 = b.i1; }
-  } else {
-    r.v1 = b.v1; r.i1 = b.i1;
-    if (better(a.v1, a.i1, b.v2, b.i2)) { r.v2 = a.v1; r.i2 = a.i1; } else { r.v2 = b.v2; r.i2 = b.i2; }
-  }
-  return r;
-}
-__device__ __forceinline__ Top2 t2_shfl(const Top2& t, int off) {
-  Top2 o;
-  o.v1 = __shfl_xor_sync(0xffffffffu, t.v1, off);
-  o.i1 = __shfl_xor_sync(0xffffffffu, t.i1, off);
-  o.v2 = __shfl_xor_sync(0xffffffffu, t.v2, off);
-  o.i2 = __shfl_xor_sync(0xffffffffu, t.i2, off);
-  return o;
-}
-
 int top2_blocks(int V) {
   int nb = (V + 8191) / 8192;
   return nb < 1 ? 1 : (nb > 64 ? 64 : nb);
@@ -117,6 +76,40 @@ cudaError_t launch_top2(const float* logits, int T, int V, float* part, int nb, 
   cudaError_t e = launch_k(k_top2_partial, g1, dim3(256), 0, st, logits, V, nb, part, nan_flag);
   if (e != cudaSuccess) return e;
   return launch_k(k_top2_final, dim3(T), dim3(32), 0, st, (const float*)part, nb, v1, i1, v2, i2, g);
+}
+
+// merge of the per-tile top-2 sets written by the LM head's fused epilogue:
+// CTA per token, 256 threads, strided merge then warp and CTA trees
+__global__ void __launch_bounds__(256) k_top2_tiles(const float* __restrict__ t2, int nt, float* v1, int32_t* i1,
+                                                    float* v2, int32_t* i2, float* g) {
+  griddep();
+  __shared__ Top2 sm[8];
+  const int t = blockIdx.x;
+  const float4* p = reinterpret_cast<const float4*>(t2) + (size_t)t * nt;
+  Top2 r{-INFINITY, INT_MAX, -INFINITY, INT_MAX};
+  for (int j = threadIdx.x; j < nt; j += 256) {
+    const float4 q = p[j];
+    r = t2_merge(r, Top2{q.x, __float_as_int(q.y), q.z, __float_as_int(q.w)});
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) r = t2_merge(r, t2_shfl(r, off));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = r;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Top2 a = sm[0];
+    for (int w = 1; w < 8; ++w) a = t2_merge(a, sm[w]);
+    if (v1) v1[t] = a.v1;
+    if (i1) i1[t] = a.i1;
+    if (v2) v2[t] = a.v2;
+    if (i2) i2[t] = a.i2;
+    if (g) g[t] = __fsub_rn(a.v1, a.v2);
+  }
+}
+
+cudaError_t launch_top2_tiles(const float* t2, int T, int nt, float* v1, int32_t* i1, float* v2, int32_t* i2,
+                              float* g, cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  return launch_k(k_top2_tiles, dim3(T), dim3(256), 0, st, t2, nt, v1, i1, v2, i2, g);
 }
 
 // ------------------------------------------------------------------ gate

@@ -283,6 +283,7 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   c->attn_cnt = s.take<int32_t>((size_t)Tm * c->KV);
   c->chain_sync = s.take<uint32_t>(2 * kChainMax + 1);
   c->top2_part = s.take<float>(Tlm * c->nb_top2 * 4);
+  c->t2tiles = s.take<float>(Tlm * (size_t)(c->V / 128) * 4);
   c->rope_cos = s.take<float>((size_t)g.max_seq * (c->hd / 2));
   c->rope_sin = s.take<float>((size_t)g.max_seq * (c->hd / 2));
   c->pos_d = s.take<int32_t>(g.max_slots);
@@ -369,7 +370,8 @@ static cudaEvent_t tevent(mg_ctx* c) {
   return t.pool[t.used++];
 }
 
-static mg_status gemm(mg_ctx* c, const uint16_t* X, int xrows, int T, const Weight& W, const OpSched& o, float* out) {
+static mg_status gemm(mg_ctx* c, const uint16_t* X, int xrows, int T, const Weight& W, const OpSched& o, float* out,
+                      float* t2 = nullptr) {
   size_t i0 = 0;
   if (c->timing.on) {
     i0 = c->timing.used;
@@ -380,7 +382,8 @@ static mg_status gemm(mg_ctx* c, const uint16_t* X, int xrows, int T, const Weig
   } else {
     const CUtensorMap* mx = xmap(c, X, W.K, xrows, o.tile_n);
     if (!mx) return fail(c, MG_ERR_CUDA, "cuTensorMapEncodeTiled failed for activations");
-    CK(launch_gemm_tc(W.map, *mx, W.N, W.K, T, o.splits, o.G, o.tile_n, o.mma_n, out, c->st));
+    CK(launch_gemm_tc(W.map, *mx, W.N, W.K, T, o.splits, o.G, o.tile_n, o.mma_n, out, c->st, t2,
+                      t2 ? c->nan_d : nullptr));
   }
   c->launches += 1;
   if (c->timing.on) {
@@ -615,10 +618,23 @@ static mg_status forward_chain(mg_ctx* c, int T, const int32_t* slot, const int3
   return MG_OK;
 }
 
+// The fused top-2 epilogue replaces the fp32 logits unless something needs
+// them: logit captures (tests), the test-only injected noise, the CUDA-core GEMV.
+static bool lm_fused(const mg_ctx* c, const OpSched& o, bool fast_rows) {
+  return o.impl == 0 && !c->capture && !c->capture_v && !(fast_rows && c->inj_amp > 0.f) && !c->lm_unfused;
+}
+
 // LM head + top-2 over the final-normed rows xnorm[0..T)
 static mg_status lm_head(mg_ctx* c, const uint16_t* xnorm, int xrows, int T, const OpSched& o, float* v1,
                          int32_t* i1, float* v2, int32_t* i2, float* g, const int32_t* inj_slot = nullptr,
                          const int32_t* inj_pos = nullptr) {
+  if (lm_fused(c, o, inj_slot != nullptr)) {  // top-2 fused into the LM head's epilogue: no logits in HBM
+    mg_status r = gemm(c, xnorm, xrows, T, c->lm, o, c->logits, c->t2tiles);
+    if (r) return r;
+    CK(launch_top2_tiles(c->t2tiles, T, c->V / 128, v1, i1, v2, i2, g, c->st));
+    c->launches++;
+    return MG_OK;
+  }
   mg_status r = gemm(c, xnorm, xrows, T, c->lm, o, c->logits);
   if (r) return r;
   if (inj_slot && c->inj_amp > 0.f) {  // test-only SPEC.md:76-84 perturbation of the fast rows
@@ -918,7 +934,20 @@ static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const 
     CK(launch_lm_rows(c->xn, B, c->last_d, c->ctrl_d, n_lm, c->d, c->xlm, c->st));
     c->launches++;
     const int T = B + n_lm;
-    if ((rr = gemm(c, c->xlm, 2 * c->cfg.max_batch, T, c->lm, op_lm(c->V, c->d, T, true), c->logits))) return rr;
+    const OpSched olm = op_lm(c->V, c->d, T, true);
+    if (lm_fused(c, olm, true)) {  // top-2 fused into the LM head's epilogue
+      if ((rr = gemm(c, c->xlm, 2 * c->cfg.max_batch, T, c->lm, olm, c->logits, c->t2tiles))) return rr;
+      const int nt = c->V / 128;
+      CK(launch_top2_tiles(c->t2tiles, B, nt, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g, c->st));
+      c->launches++;
+      if (n_lm > 0) {
+        CK(launch_top2_tiles(c->t2tiles + (size_t)B * nt * 4, n_lm, nt, c->v_v1, c->v_tok, c->v_v2, c->v_i2, c->v_g,
+                             c->st));
+        c->launches++;
+      }
+      return MG_OK;
+    }
+    if ((rr = gemm(c, c->xlm, 2 * c->cfg.max_batch, T, c->lm, olm, c->logits))) return rr;
     if (c->inj_amp > 0.f) {  // test-only perturbation of the fast rows (B of them)
       CK(launch_inject(c->logits, B, c->V, c->inj_amp, c->inj_seed, c->mx_slot, c->mx_pos, c->st));
       c->launches++;
@@ -1083,7 +1112,20 @@ static mg_status decode_fused(mg_ctx* c, const int32_t* slots, int B, const uint
     CK(launch_lm_rows(c->xn, B, c->last_d, c->ctrl_d, n_lm, c->d, c->xlm, c->st));
     c->launches++;
     const int T = B + n_lm;
-    if ((rr = gemm(c, c->xlm, 2 * c->cfg.max_batch, T, c->lm, op_lm(c->V, c->d, T, true), c->logits))) return rr;
+    const OpSched olm = op_lm(c->V, c->d, T, true);
+    if (lm_fused(c, olm, true)) {  // top-2 fused into the LM head's epilogue
+      if ((rr = gemm(c, c->xlm, 2 * c->cfg.max_batch, T, c->lm, olm, c->logits, c->t2tiles))) return rr;
+      const int nt = c->V / 128;
+      CK(launch_top2_tiles(c->t2tiles, B, nt, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g, c->st));
+      c->launches++;
+      if (n_lm > 0) {
+        CK(launch_top2_tiles(c->t2tiles + (size_t)B * nt * 4, n_lm, nt, c->v_v1, c->v_tok, c->v_v2, c->v_i2, c->v_g,
+                             c->st));
+        c->launches++;
+      }
+      return MG_OK;
+    }
+    if ((rr = gemm(c, c->xlm, 2 * c->cfg.max_batch, T, c->lm, olm, c->logits))) return rr;
     if (c->inj_amp > 0.f) {  // test-only perturbation of the fast rows (B of them)
       CK(launch_inject(c->logits, B, c->V, c->inj_amp, c->inj_seed, c->mx_slot, c->mx_pos, c->st));
       c->launches++;
@@ -1208,6 +1250,8 @@ mg_status mg_init(const mg_config* cfg, const mg_buffers* bufs, void* stream, mg
     // (DESIGN.md section 7.4); MG_CHAIN=1 selects it for A/B measurements
     const char* e = getenv("MG_CHAIN");
     c->use_chain = e && e[0] == '1';
+    const char* lu = getenv("MG_LM_UNFUSED");  // A/B knob: logits + separate top-2 kernels
+    c->lm_unfused = lu && lu[0] == '1';
     const char* fs = getenv("MG_FAST_SK");  // measurement knobs: attention split sizes
     c->fast_sk_override = fs ? atoi(fs) : 0;
     const char* f = getenv("MG_CHAIN_PF");  // A/B knob: L2 run-ahead in 16 KB k-blocks

@@ -75,6 +75,7 @@ struct mg_ctx {
   // workspace
   uint16_t *x, *xn, *q, *att, *a, *xg, *xgn;
   float *part, *logits, *attn_acc, *attn_ml, *top2_part;
+  float* t2tiles = nullptr;  // fused LM-head top-2: per-(token, 128-row tile) sets [Tlm][V/128][4]
   int32_t* attn_cnt;                     // [Tmax][KV] chunk-arrival counters
   uint32_t* chain_sync;                  // layer-chain grid barriers + epoch (chain.h)
   bool use_chain = false;                // MG_CHAIN=1: persistent layer chain (A/B only; slower today)
@@ -92,6 +93,7 @@ struct mg_ctx {
   bool f_sync = false;       // a pipelined step's readback is in flight
   std::vector<char> pend_h;
   int fast_mode = 0;         // mg_fast_schedule (mg_set_policy)
+  bool lm_unfused = false;   // MG_LM_UNFUSED=1: fp32 logits + separate top-2 (A/B measurement)
   float inj_amp = 0.f;       // test-only logit perturbation (mgd_set_inject)
   unsigned long long inj_seed = 0;
   int force_B = 0;           // test-only: fast attention splits of another batch size (mgd_force_schedule)

@@ -33,6 +33,8 @@
 // choice): warp per output row, 128-bit weight loads, fp32 FMA, fixed
 // xor-shuffle tree.
 #include "common.cuh"
+#include <climits>
+
 #include "gemm_tc.cuh"
 #include "kernels.h"
 
@@ -160,6 +162,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     if (ctr && lane == 0) ctr[2] = (long long)globaltimer();
   } else {  // ---- epilogue warps 2..5: TMEM lanes 32*(warp%4) ..
+    __shared__ Top2 s_t2[4][16];  // fused top-2: per-warp results of one 16-token chunk
     griddep_wait();
     const int q = warp & 3;
     int j = 0;
@@ -179,6 +182,31 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t r[16];
         tc_ld_32x32b_x16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * C::ACC_COLS + c0), r);
         tc_wait_ld();
+        if (g.t2) {
+          // fused top-2 over this tile's 128 rows for each of the 16 tokens:
+          // warp shuffle tree over its 32 rows, then the 4 warps through smem
+          bool nan = false;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float v = __uint_as_float(r[i]);
+            if (v != v) { nan = true; v = -INFINITY; }
+            Top2 tt{v, n, -INFINITY, INT_MAX};
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) tt = t2_merge(tt, t2_shfl(tt, off));
+            if (lane == 0) s_t2[q][i] = tt;
+          }
+          if (nan) atomicOr(g.nan_flag, 1);
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (q == 0 && lane < 16 && t0 + c0 + lane < g.T) {
+            Top2 a = s_t2[0][lane];
+#pragma unroll
+            for (int w = 1; w < 4; ++w) a = t2_merge(a, s_t2[w][lane]);
+            float* dst = g.t2 + ((size_t)(t0 + c0 + lane) * g.n_m + pc.mt) * 4;
+            *reinterpret_cast<float4*>(dst) = make_float4(a.v1, __int_as_float(a.i1), a.v2, __int_as_float(a.i2));
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          continue;
+        }
         if (!(g.dbg & 2)) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -313,7 +341,7 @@ int num_sms() {
 
 template <int TN, bool MMA16>
 static cudaError_t launch_tc_t(const CUtensorMap& mw, const CUtensorMap& mx, int N, int K, int T, int splits, int G,
-                               float* out, cudaStream_t st) {
+                               float* out, cudaStream_t st, float* t2, int32_t* nan_flag) {
   using C = GemmTcCfg<TN>;
   static bool attr = false;
   if (!attr) {
@@ -328,6 +356,9 @@ static cudaError_t launch_tc_t(const CUtensorMap& mw, const CUtensorMap& mx, int
   g.G = G;
   g.dbg = g_gemm_dbg;
   g.out = out;
+  g.t2 = t2;
+  g.nan_flag = nan_flag;
+  if (t2 && (G != 0 || g.splits != 1 || !nan_flag)) return cudaErrorInvalidValue;
   const int work = G > 0 ? G * g.n_t : g.units;
   const int grid = work < num_sms() ? work : num_sms();
   return launch_k(k_gemm_tc<TN, MMA16>, dim3(grid), dim3(C::THREADS), C::SMEM, st, mw, mx, g);
@@ -335,20 +366,20 @@ static cudaError_t launch_tc_t(const CUtensorMap& mw, const CUtensorMap& mx, int
 
 template <int TN>
 static cudaError_t launch_tc_m(const CUtensorMap& mw, const CUtensorMap& mx, int N, int K, int T, int splits, int G,
-                               int mma_n, float* out, cudaStream_t st) {
-  if (mma_n == 16 && TN > 16) return launch_tc_t<TN, true>(mw, mx, N, K, T, splits, G, out, st);
-  return launch_tc_t<TN, false>(mw, mx, N, K, T, splits, G, out, st);
+                               int mma_n, float* out, cudaStream_t st, float* t2, int32_t* nan_flag) {
+  if (mma_n == 16 && TN > 16) return launch_tc_t<TN, true>(mw, mx, N, K, T, splits, G, out, st, t2, nan_flag);
+  return launch_tc_t<TN, false>(mw, mx, N, K, T, splits, G, out, st, t2, nan_flag);
 }
 
 cudaError_t launch_gemm_tc(const CUtensorMap& mw, const CUtensorMap& mx, int N, int K, int T, int splits, int G,
-                           int tile_n, int mma_n, float* out, cudaStream_t st) {
+                           int tile_n, int mma_n, float* out, cudaStream_t st, float* t2, int32_t* nan_flag) {
   if (mma_n != 16) mma_n = tile_n;
   switch (tile_n) {
-    case 16: return launch_tc_m<16>(mw, mx, N, K, T, splits, G, mma_n, out, st);
-    case 32: return launch_tc_m<32>(mw, mx, N, K, T, splits, G, mma_n, out, st);
-    case 64: return launch_tc_m<64>(mw, mx, N, K, T, splits, G, mma_n, out, st);
-    case 128: return launch_tc_m<128>(mw, mx, N, K, T, splits, G, mma_n, out, st);
-    case 256: return launch_tc_m<256>(mw, mx, N, K, T, splits, G, mma_n, out, st);
+    case 16: return launch_tc_m<16>(mw, mx, N, K, T, splits, G, mma_n, out, st, t2, nan_flag);
+    case 32: return launch_tc_m<32>(mw, mx, N, K, T, splits, G, mma_n, out, st, t2, nan_flag);
+    case 64: return launch_tc_m<64>(mw, mx, N, K, T, splits, G, mma_n, out, st, t2, nan_flag);
+    case 128: return launch_tc_m<128>(mw, mx, N, K, T, splits, G, mma_n, out, st, t2, nan_flag);
+    case 256: return launch_tc_m<256>(mw, mx, N, K, T, splits, G, mma_n, out, st, t2, nan_flag);
     default: return cudaErrorInvalidValue;
   }
 }

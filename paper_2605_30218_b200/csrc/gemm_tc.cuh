@@ -42,6 +42,12 @@ struct GemmArgs {
   int G;    // > 0: stream-K over G virtual CTAs per token tile; 0: uniform split-K
   int dbg;  // microbenchmark knobs (0 in the product): 1 skip MMAs, 2 skip stores, 1024 trace CTA 0
   float* out;
+  // fused top-1/top-2 epilogue (LM head, "computes only the top
+  // two values"): instead of the fp32 logits, each 128-row tile writes, per
+  // token, its top-2 (v1, i1, v2, i2) to t2[t][n_m][4]; NaN ranks as -inf and
+  // sets *nan_flag.  Requires a single piece per tile (G == 0, splits == 1).
+  float* t2;
+  int32_t* nan_flag;
 };
 
 // A piece = one contiguous k-block range of one 128-feature tile for one

@@ -60,8 +60,10 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, int inner_k, int rows, int b
 // splits: uniform split-K (G == 0) or ignored; G > 0: stream-K over G
 // virtual CTAs per token tile (partial slots per tile: part_count()).
 // tile_n in {16, 32, 64, 128, 256}; mma_n 16 (verifier slot groups) or tile_n
+// t2 != nullptr: fused top-2 epilogue (GemmArgs::t2; LM head only: G == 0, splits == 1)
 cudaError_t launch_gemm_tc(const CUtensorMap& mw, const CUtensorMap& mx, int N, int K, int T, int splits, int G,
-                           int tile_n, int mma_n, float* out, cudaStream_t st);
+                           int tile_n, int mma_n, float* out, cudaStream_t st, float* t2 = nullptr,
+                           int32_t* nan_flag = nullptr);
 // max partial slots of any tile for a GEMM shape (buffer sizing)
 int part_slots(const PartSpec& p, int N);
 int num_sms();
@@ -155,6 +157,9 @@ cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st);
 // ---- top-2, gate, catch-up, commit (a8-a11)
 cudaError_t launch_top2(const float* logits, int T, int V, float* part /*[T][nb][4]*/, int nb, float* v1, int32_t* i1,
                         float* v2, int32_t* i2, float* g, int32_t* nan_flag, cudaStream_t st);
+// merge of the fused LM-head epilogue's per-tile top-2 sets t2 [T][nt][4] -> v1, i1, v2, i2, g = v1 - v2
+cudaError_t launch_top2_tiles(const float* t2, int T, int nt, float* v1, int32_t* i1, float* v2, int32_t* i2,
+                              float* g, cudaStream_t st);
 int top2_blocks(int V);
 
 }  // namespace mg

@@ -393,3 +393,37 @@ def test_force_schedule_reproduces_batch_shape(torch, tiny):
         eng.close()
     for a, b in zip(*caps):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("B,mode", [(6, 0), (6, 2), (1, 0)])
+def test_fused_lm_top2_equals_logits_path(torch, tiny, B, mode):
+    """The LM head's fused top-2 epilogue (per-tile top-2 in the tcgen05 GEMM
+    epilogue, then a merge over the tiles) gives bit-identical (v1, i1, v2, i2,
+    g) to the fp32-logits + top-2 kernels (MG_LM_UNFUSED=1), for the fast rows
+    and the verifier rows: the top-2 under (value desc, id asc) is exact, so
+    the merge order cannot matter."""
+    import os
+    shp, _ = tiny
+    prompts = inputs.prompts(B, inputs.ragged_lengths(B, 8, 23, seed=61), shp["vocab"], seed=390)
+    recs = []
+    for unfused in ("1", "0"):
+        os.environ["MG_LM_UNFUSED"] = unfused
+        try:
+            eng = _engine(shp, B)
+        finally:
+            del os.environ["MG_LM_UNFUSED"]
+        eng.set_policy(verify_mode=mode)
+        for i, p in enumerate(prompts):
+            eng.prefill(i, p)
+        out = torch.empty(B, dtype=torch.int32, device="cuda")
+        rr = []
+        for _ in range(8):
+            eng.step(list(range(B)), None, INF, out)
+            r = eng.last_step(B)
+            rr.append((r["f_tok"].copy(), r["g"].copy(), r["v1"].copy(), r["v2"].copy(), r["v_tok"].copy(),
+                       r["v_g"].copy(), out.cpu().numpy().copy()))
+        recs.append(rr)
+        eng.close()
+    for a, b in zip(*recs):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
