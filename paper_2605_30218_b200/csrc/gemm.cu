@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(192, 1)
     }
     if (ctr && lane == 0) ctr[2] = (long long)globaltimer();
   } else {  // ---- epilogue warps 2..5: TMEM lanes 32*(warp%4) ..
-    __shared__ Top2 s_t2[4][16];  // fused top-2: per-warp results of one 16-token chunk
+    __shared__ Top2 s_t2[4][16];         // fused top-2: per-warp results of one 16-token chunk
+    __shared__ float s_val[4][16 * 33];  // fused top-2: per-warp [token][row] transpose (padded)
     griddep_wait();
     const int q = warp & 3;
     int j = 0;
@@ -184,18 +185,28 @@ __global__ void __launch_bounds__(192, 1)
         tc_wait_ld();
         if (g.t2) {
           // fused top-2 over this tile's 128 rows for each of the 16 tokens:
-          // warp shuffle tree over its 32 rows, then the 4 warps through smem
+          // each warp transposes its 32 rows x 16 tokens through shared memory,
+          // lane (token i, half h) scans 16 rows, one shuffle merges the halves;
+          // then the 4 warps merge through s_t2
           bool nan = false;
+          float* sv = s_val[q];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float v = __uint_as_float(r[i]);
             if (v != v) { nan = true; v = -INFINITY; }
-            Top2 tt{v, n, -INFINITY, INT_MAX};
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) tt = t2_merge(tt, t2_shfl(tt, off));
-            if (lane == 0) s_t2[q][i] = tt;
+            sv[i * 33 + lane] = v;
           }
           if (nan) atomicOr(g.nan_flag, 1);
+          __syncwarp();
+          {
+            const int i = lane & 15, h = lane >> 4;
+            const int id0 = pc.mt * C::BM + q * 32 + h * 16;
+            Top2 tt{-INFINITY, INT_MAX, -INFINITY, INT_MAX};
+#pragma unroll
+            for (int rr = 0; rr < 16; ++rr) t2_push(tt, sv[i * 33 + h * 16 + rr], id0 + rr);
+            tt = t2_merge(tt, t2_shfl(tt, 16));
+            if (lane < 16) s_t2[q][i] = tt;
+          }
           asm volatile("bar.sync 1, 128;" ::: "memory");
           if (q == 0 && lane < 16 && t0 + c0 + lane < g.T) {
             Top2 a = s_t2[0][lane];
