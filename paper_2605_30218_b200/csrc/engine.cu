@@ -862,18 +862,9 @@ static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const 
       return fail(c, MG_ERR_STATE, "a slot with a pending tentative token is missing from the batch "
                                    "(include it or call mg_verify_window)");
   if ((int)c->free_pages.size() < need_pages) return fail(c, MG_ERR_CAPACITY, "KV pages exhausted");
-  // the pending list built at the end of the previous step (device ctrl / last / cu_*)
-  const int32_t* ctrl_h = c->fpin;
   int n_pend = 0, M = 0, vmax = 1;
   std::vector<int> last;
   for (int s = 0; s < S; ++s) n_pend += c->active[s] && c->pend_h[s];
-  if (n_pend > 0) {
-    if (ctrl_h[0] != n_pend) return fail(c, MG_ERR_CUDA, "pending list mismatch between host mirror and device");
-    M = ctrl_h[1];
-    last.assign(ctrl_h + 2 + c->cfg.max_batch, ctrl_h + 2 + c->cfg.max_batch + n_pend);
-    for (int s = 0; s < S; ++s)
-      if (c->active[s] && c->pend_h[s] && c->pos_h[s] > vmax) vmax = c->pos_h[s];
-  }
   size_t ev0 = 0;
   if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
   // upload batch + protection mask + page-table updates (as mg_decode_step)
@@ -901,6 +892,32 @@ static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const 
       CK(cudaGetLastError());
       c->launches++;
     }
+  }
+  // the pending list built at the end of the previous step (device ctrl / last / cu_*);
+  // rebuilt here (pending-list gate over this batch) when mg_verify_window or
+  // mg_release changed the pending set since
+  const int32_t* ctrl_h = c->fpin;
+  if (n_pend > 0 && c->pend_dirty) {
+    GateArgs gp{};
+    gp.g = c->f_g; gp.prot = c->prot_d; gp.tau = tau; gp.slots = c->slots_d; gp.B = B;
+    gp.pos = c->pos_d; gp.shadow_len = c->shadow_d; gp.hist = c->hist_d; gp.hist_stride = c->cfg.max_seq + 1;
+    gp.trig = c->trig_d; gp.rank = c->rank_d; gp.ctrl = c->ctrl_d; gp.last = c->last_d;
+    gp.cu_slot = c->cu_slot; gp.cu_pos = c->cu_pos; gp.cu_tok = c->cu_tok; gp.cu_nk = c->cu_nk;
+    gp.pend = c->pend_d; gp.rank_slot = c->rank_slot_d;
+    CK(launch_gate(gp, c->st));
+    c->launches++;
+    const int MB = c->cfg.max_batch;
+    CK(cudaMemcpyAsync(c->fpin, c->ctrl_d, (2 + B) * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(c->fpin + 2 + MB, c->last_d, B * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
+  c->pend_dirty = false;
+  if (n_pend > 0) {
+    if (ctrl_h[0] != n_pend) return fail(c, MG_ERR_CUDA, "pending list mismatch between host mirror and device");
+    M = ctrl_h[1];
+    last.assign(ctrl_h + 2 + c->cfg.max_batch, ctrl_h + 2 + c->cfg.max_batch + n_pend);
+    for (int s = 0; s < S; ++s)
+      if (c->active[s] && c->pend_h[s] && c->pos_h[s] > vmax) vmax = c->pos_h[s];
   }
   // catch-up too long to ride along: the pending rows' verifier runs on its own first
   int Mx = M;
@@ -1521,6 +1538,7 @@ mg_status mg_verify_window(mg_ctx* c, const int32_t* slots, int32_t n, int32_t* 
     const int s = slots[i];
     c->pos_h[s] = res[3 * i];
     c->shadow_h[s] = res[3 * i];
+    if (c->pend_h[s]) c->pend_dirty = true;
     c->pend_h[s] = 0;
     if (pos_out) pos_out[i] = res[3 * i];
     if (last_out) last_out[i] = res[3 * i + 1];
@@ -1557,6 +1575,7 @@ mg_status mg_release(mg_ctx* c, int32_t slot) {
   if (c->pend_h[slot]) {
     CK(cudaMemsetAsync(c->pend_d + slot, 0, 1, c->st));
     c->pend_h[slot] = 0;
+    c->pend_dirty = true;
   }
   for (int p : c->pages[slot]) c->free_pages.push_back(p);
   c->pages[slot].clear();

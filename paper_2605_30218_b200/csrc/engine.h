@@ -91,6 +91,7 @@ struct mg_ctx {
   int32_t* fpin = nullptr;   // pinned readback of a pipelined step: ctrl | last | pos | shadow | pend
   cudaEvent_t fev = nullptr;
   bool f_sync = false;       // a pipelined step's readback is in flight
+  bool pend_dirty = false;   // pending set changed outside a step (mg_verify_window / mg_release)
   std::vector<char> pend_h;
   int fast_mode = 0;         // mg_fast_schedule (mg_set_policy)
   bool lm_unfused = false;   // MG_LM_UNFUSED=1: fp32 logits + separate top-2 (A/B measurement)

@@ -427,3 +427,55 @@ def test_fused_lm_top2_equals_logits_path(torch, tiny, B, mode):
     for a, b in zip(*recs):
         for x, y in zip(a, b):
             assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_slot_churn_tau_inf_is_reference(torch, tiny, mode):
+    """Continuous batching: requests leave (mg_release) and new ones are
+    prefilled into the freed slots while the others keep decoding; at tau=inf
+    every request's committed sequence equals its own batch-1 reference in
+    the synchronous, pipelined and fused verify modes (the verifier depends
+    only on the request's prefix)."""
+    shp, _ = tiny
+    S, B, steps = 8, 5, 36
+    reqs = inputs.prompts(12, inputs.ragged_lengths(12, 6, 20, seed=71), shp["vocab"], seed=400)
+    eng = _engine(shp, S)
+    eng.set_policy(verify_mode=mode)
+    out = torch.empty(S, dtype=torch.int32, device="cuda")
+    kind = torch.empty(S, dtype=torch.uint8, device="cuda")
+    live, done, nxt = {}, {}, 0          # slot -> (request, sequence)
+    for s in range(B):
+        live[s] = (nxt, [eng.prefill(s, reqs[nxt])])
+        nxt += 1
+    for step in range(steps):
+        slots = sorted(live)
+        eng.step(slots, None, INF, out[:len(slots)], kind[:len(slots)])
+        o, k = out.cpu().numpy(), kind.cpu().numpy()
+        for j, s in enumerate(slots):
+            seq = live[s][1]
+            if mode == 1 and k[j] == 4:
+                seq[-1] = int(o[j])
+            else:
+                seq.append(int(o[j]))
+        if step % 6 == 5 and nxt < len(reqs):      # one request leaves, a new one joins a free slot
+            s = slots[step // 6 % len(slots)]
+            r, seq = live.pop(s)
+            pos, last, _ = eng.verify_window([s])   # resolve a tentative token (pipelined) before leaving
+            n = int(pos[0]) - len(reqs[r]) + 1
+            done[r] = seq[:n - 1] + [int(last[0])]
+            eng.release(s)
+            free = [x for x in range(S) if x not in live and x != s]
+            live[free[0]] = (nxt, [eng.prefill(free[0], reqs[nxt])])
+            nxt += 1
+    slots = sorted(live)
+    pos, last, _ = eng.verify_window(slots)
+    for j, s in enumerate(slots):
+        r, seq = live[s]
+        n = int(pos[j]) - len(reqs[r]) + 1
+        done[r] = seq[:n - 1] + [int(last[j])]
+    eng.close()
+    for r, seq in done.items():
+        e1 = _engine(shp, 1)
+        ref = _decode(torch, e1, [reqs[r]], len(seq), INF)[0]
+        e1.close()
+        assert seq == ref, (mode, r)
