@@ -81,3 +81,12 @@ def test_null_ctx_calls_are_invalid():
     assert L.mg_release(None, 0) == _lib.MG_ERR_INVALID
     assert L.mg_decode_step(None, None, 1, None, 0.0, None, None, None) == _lib.MG_ERR_INVALID
     L.mg_destroy(None)  # no-op
+
+
+def test_graft_entry_imports():
+    """The driver's entry module parses and exposes build() / smoke()."""
+    import importlib
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    m = importlib.import_module("__graft_entry__")
+    assert callable(m.build) and callable(m.smoke)
