@@ -310,9 +310,23 @@ def run_gpu(args):
     # ---- the paper's own protocol: batch 8, one
     # protected request, tau100 calibrated on disjoint seeds -- the regime
     # where the fast path's schedule really differs from the verifier's
+    # ---- LLM-42-style windowed verify + rollback at the headline batch (NEXT-2;
+    # K = --window, two windows), one and all rows protected, on an engine with
+    # room for the extra positions (rank-local timing, like the paper arm)
+    w64 = None
+    if not args.quick and args.window > 0:
+        eng.close()
+        ew = Engine(shp, max_batch=B, max_slots=B, max_seq=ctx0 + W + 2 * args.window + 2, page_size=64)
+        w64 = {}
+        for pname, pm in (("one", prot_one), ("all", prot_all)):
+            w64[pname] = _window_run(ew, prompts, pm, W, 2 * args.window, args.window)
+        ew.close()
+        eng = None
+
     paper = None
     if not args.quick and args.paper_batch > 0:
-        eng.close()
+        if eng is not None:
+            eng.close()
         pb = args.paper_batch
         e8 = Engine(shp, max_batch=pb, max_slots=pb, max_seq=ctx0 + W + max(K, 2 * args.window) + 2, page_size=64)
         cal8 = calibrate(e8, inputs.prompts(pb, ctx0, shp["vocab"], seed=1000 + rank * pb), 3, K)
@@ -424,6 +438,12 @@ def run_gpu(args):
         "determinism_pct": round(100 * df[0] / df[1], 2) if df[1] else None,
         "note": "MG_VERIFY_FUSED: every protected row's verifier token computed speculatively in the same "
                 "weight pass; the gate selects which to commit (synchronous semantics)"}
+    if w64 is not None:
+        arms_out["llm42_window"] = {
+            p: {"window": args.window, "steps": 2 * args.window, "tok_s": round(v[1] / (v[2] * 1e-3), 2),
+                "inc": round((v[2] / v[1]) / (T["bf16"] / (B * K)) - 1, 4), **v[3],
+                "note": "rank 0; inc per net committed token vs the BF16 arm per token"}
+            for p, v in w64.items()}
     if "mg_other" in res:
         arms_out["other"] = summary("mg_other", "ao_other", do, other)
         arms_out["other"]["pipelined"] = pipe("ao_pipe_other", other, None)
