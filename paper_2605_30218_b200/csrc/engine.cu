@@ -519,7 +519,8 @@ static mg_status forward_mixed(mg_ctx* c, int B, int M, const Sched& fs, const S
 static bool chain_ok(const mg_ctx* c, const Sched& sc) {
   const OpSched* ops[4] = {&sc.qkv, &sc.o, &sc.gu, &sc.down};
   for (const OpSched* o : ops)
-    if (o->impl != 0 || o->G < 1 || o->tile_n != sc.qkv.tile_n || o->mma_n != sc.qkv.mma_n) return false;
+    if (o->impl != 0 || o->G < 1 || o->tile_n != sc.qkv.tile_n || o->mma_n != sc.qkv.mma_n || o->tile_n == 80)
+      return false;  // the layer chain is instantiated for power-of-two tiles only
   return c->use_chain;
 }
 

@@ -389,6 +389,7 @@ cudaError_t launch_gemm_tc(const CUtensorMap& mw, const CUtensorMap& mx, int N, 
     case 16: return launch_tc_m<16>(mw, mx, N, K, T, splits, G, mma_n, out, st, t2, nan_flag);
     case 32: return launch_tc_m<32>(mw, mx, N, K, T, splits, G, mma_n, out, st, t2, nan_flag);
     case 64: return launch_tc_m<64>(mw, mx, N, K, T, splits, G, mma_n, out, st, t2, nan_flag);
+    case 80: return launch_tc_m<80>(mw, mx, N, K, T, splits, G, mma_n, out, st, t2, nan_flag);
     case 128: return launch_tc_m<128>(mw, mx, N, K, T, splits, G, mma_n, out, st, t2, nan_flag);
     case 256: return launch_tc_m<256>(mw, mx, N, K, T, splits, G, mma_n, out, st, t2, nan_flag);
     default: return cudaErrorInvalidValue;
@@ -408,6 +409,7 @@ int gemm_tile_n(int T) {
   if (T <= 16) return 16;
   if (T <= 32) return 32;
   if (T <= 64) return 64;
+  if (T <= 80) return 80;  // e.g. a batch of 64 plus the fused verifier's columns: 4 stages, not the 128 tile's 3
   if (T <= 128) return 128;
   return 256;
 }

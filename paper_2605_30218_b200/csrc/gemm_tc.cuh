@@ -27,10 +27,12 @@ struct GemmTcCfg {
   static constexpr int A_BYTES = KS * A_BOX;
   static constexpr int B_BYTES = KS * B_BOX;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int NS0 = (MG_GEMM_SMEM_KB * 1024) / STAGE;
+  // the 80-token tile (a batch of 64 plus the fused verifier's columns) gets
+  // 208 KB so it keeps 4 stages (128 KB of weights in flight) like the 64 tile
+  static constexpr int NS0 = ((TN == 80 ? 208 : MG_GEMM_SMEM_KB) * 1024) / STAGE;
   static constexpr int NS = NS0 > MG_GEMM_NS_MAX ? MG_GEMM_NS_MAX : NS0;
-  static constexpr int ACC_COLS = TN < 32 ? 32 : TN;
-  static constexpr int TMEM_COLS = 2 * ACC_COLS;
+  static constexpr int ACC_COLS = TN < 32 ? 32 : (TN + 31) / 32 * 32;  // accumulator columns (32-aligned)
+  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 64 ? 64 : (2 * ACC_COLS <= 128 ? 128 : (2 * ACC_COLS <= 256 ? 256 : 512));
   static constexpr int THREADS = 192;
   static constexpr int SMEM = 1024 + NS * STAGE + (2 * NS + 4) * 8 + 16;
   static_assert(NS >= 2, "pipeline needs two stages");

@@ -81,7 +81,8 @@ def _check_gemm(orc, x, W, part, counts=None):
 @pytest.mark.parametrize("T,N,K_,splits,mma_n,tile_n", [
     (1, 128, 64, 1, 0, 16), (5, 256, 256, 1, 0, 16), (16, 384, 512, 2, 16, 16), (17, 256, 256, 1, 0, 32),
     (48, 128, 1024, 3, 16, 64), (64, 512, 4096, 7, 0, 64), (64, 512, 4096, 7, 16, 64), (100, 256, 768, 1, 16, 128),
-    (256, 128, 256, 1, 0, 256), (300, 256, 512, 2, 16, 256), (96, 128, 14336, 16, 0, 128), (3, 128, 192, 3, 0, 16)])
+    (256, 128, 256, 1, 0, 256), (300, 256, 512, 2, 16, 256), (96, 128, 14336, 16, 0, 128), (3, 128, 192, 3, 0, 16),
+    (65, 256, 1024, 1, 0, 80), (80, 384, 4096, 5, 16, 80), (170, 128, 512, 2, 0, 80)])
 def test_gemm_tcgen05(orc, K, T, N, K_, splits, mma_n, tile_n):
     rng = np.random.default_rng(T * 131 + N + K_)
     x = _rand(orc, rng, (T, K_))
@@ -154,7 +155,7 @@ def test_gemm_column_invariance(orc, K):
             for col in sorted(c for c in {0, 1, 15, T // 2, T - 1} if c < T):
                 x = others.copy()
                 x[col] = target[0]
-                for tile in (16, 32, 64, 128, 256):
+                for tile in (16, 32, 64, 80, 128, 256):
                     for mma in sorted({16, tile}):
                         part = K.gemm(x, W, splits=splits, impl=0, mma_n=mma, tile_n=tile)
                         ok = np.isnan(ref) == np.isnan(part[:, col])
