@@ -133,3 +133,50 @@ def test_full_size_sampled_row_parity(orc, name):
     A.close()
     D.close()
     m.close()
+
+
+def test_full_size_verify_modes_agree():
+    """Llama-8B shape at bench.py's batch / capacity: the fused (same-step,
+    one weight pass) and pipelined verify modes commit exactly the
+    synchronous mode's tokens at tau = inf, every row protected (include/mg.h
+    MG_VERIFY_FUSED / MG_VERIFY_PIPELINED) -- the full-depth counterpart of
+    tests/test_gpu_next.py's tiny-model equalities."""
+    import torch
+
+    from paper_2605_30218_b200.engine import Engine
+    shp = inputs.shape("llama8b")
+    B, plen, steps = 64, 12, 5
+    prompts = inputs.prompts(B, plen, shp["vocab"], seed=4343)
+    eng = Engine(shp, max_batch=B, max_slots=B, max_seq=_bench_max_seq(), page_size=64)
+    out = torch.empty(B, dtype=torch.int32, device="cuda")
+    kind = torch.empty(B, dtype=torch.uint8, device="cuda")
+    runs = {}
+    for mode in (0, 2, 1):
+        for i in range(B):
+            try:
+                eng.release(i)
+            except Exception:
+                pass
+        eng.set_policy(verify_mode=mode)
+        seqs = [[eng.prefill(i, p)] for i, p in enumerate(prompts)]
+        for _ in range(steps):
+            eng.step(list(range(B)), None, INF, out, kind)
+            o, k = out.cpu().numpy(), kind.cpu().numpy()
+            for b in range(B):
+                if mode == 1 and k[b] == 4:
+                    seqs[b][-1] = int(o[b])
+                else:
+                    seqs[b].append(int(o[b]))
+        if mode == 1:
+            pos, last, _ = eng.verify_window(list(range(B)))
+            for b in range(B):
+                n = int(pos[b]) - plen + 1
+                del seqs[b][n:]
+                seqs[b][-1] = int(last[b])
+        eng.set_policy(verify_mode=0)
+        runs[mode] = seqs
+    eng.close()
+    assert runs[2] == runs[0]
+    for b in range(B):
+        n = min(len(runs[1][b]), len(runs[0][b]))
+        assert n >= steps - 1 and runs[1][b][:n] == runs[0][b][:n], b
