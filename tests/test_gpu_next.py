@@ -479,3 +479,44 @@ def test_slot_churn_tau_inf_is_reference(torch, tiny, mode):
         ref = _decode(torch, e1, [reqs[r]], len(seq), INF)[0]
         e1.close()
         assert seq == ref, (mode, r)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_changing_protection_mask_matches_sync(torch, tiny, mode):
+    """Per-step protection masks that change (a row unprotected for a few steps
+    then protected again, so its shadow cache catches up several positions in
+    one launch): the fused and pipelined modes commit the synchronous mode's
+    tokens (tau = 0.3, real triggers)."""
+    shp, _ = tiny
+    B, steps, tau = 6, 30, 0.3
+    prompts = inputs.prompts(B, inputs.ragged_lengths(B, 8, 23, seed=91), shp["vocab"], seed=410)
+    rng = np.random.default_rng(5)
+    masks = [(rng.random(B) < 0.5).astype(np.uint8) for _ in range(steps - 1)]
+    runs = []
+    for m in (0, mode):
+        eng = _engine(shp, B)
+        eng.set_policy(verify_mode=m)
+        seqs = [[eng.prefill(i, p)] for i, p in enumerate(prompts)]
+        out = torch.empty(B, dtype=torch.int32, device="cuda")
+        kind = torch.empty(B, dtype=torch.uint8, device="cuda")
+        for t in range(steps - 1):
+            eng.step(list(range(B)), masks[t], tau, out, kind)
+            o, k = out.cpu().numpy(), kind.cpu().numpy()
+            for b in range(B):
+                if m == 1 and k[b] == 4:
+                    seqs[b][-1] = int(o[b])
+                else:
+                    seqs[b].append(int(o[b]))
+        if m == 1:
+            pos, last, _ = eng.verify_window(list(range(B)))
+            for b in range(B):
+                n = int(pos[b]) - len(prompts[b]) + 1
+                del seqs[b][n:]
+                seqs[b][-1] = int(last[b])
+        runs.append(seqs)
+        eng.close()
+    for b in range(B):
+        n = min(len(runs[0][b]), len(runs[1][b]))
+        assert n >= steps // 2 and runs[0][b][:n] == runs[1][b][:n], b
+    if mode == 2:
+        assert runs[0] == runs[1]
