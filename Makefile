@@ -12,7 +12,13 @@ OBJS      := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(SRCS))
 LIB       := paper_2605_30218_b200/lib/libmargingate.so
 HDRS      := $(wildcard $(CSRC)/*.h $(CSRC)/*.cuh include/*.h)
 
-all: $(LIB) oracle/liboracle.so
+all: $(LIB) oracle/liboracle.so examples/mg_decode
+
+# a plain C client of the C ABI (no Python / torch): caller-owned cudaMalloc buffers
+examples/mg_decode: examples/mg_decode.c include/mg.h $(LIB)
+	gcc -O2 -std=c11 -Wall -Iinclude -I/usr/local/cuda/include -o $@ examples/mg_decode.c \
+	    -Lpaper_2605_30218_b200/lib -lmargingate -L/usr/local/cuda/lib64 -lcudart -lm \
+	    -Wl,-rpath,'$$ORIGIN/../paper_2605_30218_b200/lib' -Wl,-rpath,/usr/local/cuda/lib64
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
@@ -26,6 +32,6 @@ oracle/liboracle.so: oracle/mg_oracle.c oracle/mg_oracle.h
 	gcc -O2 -std=c11 -fPIC -shared -fopenmp -ffp-contract=off -fno-fast-math -Wall -o $@ oracle/mg_oracle.c -lm
 
 clean:
-	rm -rf $(BUILD) $(LIB) oracle/liboracle.so
+	rm -rf $(BUILD) $(LIB) oracle/liboracle.so examples/mg_decode
 
 .PHONY: all clean
