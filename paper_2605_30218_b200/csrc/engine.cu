@@ -688,6 +688,37 @@ static mg_status apply_pt(mg_ctx* c, const std::vector<std::pair<int, int>>& upd
   return MG_OK;
 }
 
+// One H2D copy per step: the batch's slots, its protection bytes (packed) and
+// the page-table entries of the pages its rows now enter; then slots_d /
+// prot_d and the page table on the device.
+static mg_status upload_batch(mg_ctx* c, const int32_t* slots, int B, const uint8_t* prot) {
+  std::vector<std::pair<int, int>> upd;
+  for (int b = 0; b < B; ++b) {
+    const int s = slots[b];
+    if (c->pos_h[s] / c->PS >= (int)c->pages[s].size()) alloc_page(c, s, &upd);
+  }
+  const int pw = (B + 3) / 4;  // prot bytes packed in words
+  std::vector<int32_t> w(B + pw + 2 * upd.size());
+  memcpy(w.data(), slots, B * 4);
+  std::vector<uint8_t> pb(pw * 4, 1);
+  if (prot) memcpy(pb.data(), prot, B);
+  memcpy(w.data() + B, pb.data(), pw * 4);
+  for (size_t i = 0; i < upd.size(); ++i) {
+    w[B + pw + 2 * i] = upd[i].first;
+    w[B + pw + 2 * i + 1] = upd[i].second;
+  }
+  mg_status r = upload(c, w);
+  if (r) return r;
+  CK(cudaMemcpyAsync(c->slots_d, c->staging_d, B * 4, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(c->prot_d, c->staging_d + B, B, cudaMemcpyDeviceToDevice, c->st));
+  if (!upd.empty()) {
+    k_apply_pt<<<cdiv((int)upd.size(), 128), 128, 0, c->st>>>(c->pt_d, c->staging_d + B + pw, (int)upd.size());
+    CK(cudaGetLastError());
+    c->launches++;
+  }
+  return MG_OK;
+}
+
 // Runs the deterministic schedule over a token list already on device
 // (cu_* arrays, entries [0, M)), in chunks of Tv tokens, then the LM head +
 // top-2 on the rows' last tokens `last_host` (list indices, ascending),
@@ -868,32 +899,7 @@ static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const 
   for (int s = 0; s < S; ++s) n_pend += c->active[s] && c->pend_h[s];
   size_t ev0 = 0;
   if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
-  // upload batch + protection mask + page-table updates (as mg_decode_step)
-  std::vector<std::pair<int, int>> upd;
-  for (int b = 0; b < B; ++b) {
-    const int s = slots[b];
-    if (c->pos_h[s] / c->PS >= (int)c->pages[s].size()) alloc_page(c, s, &upd);
-  }
-  {
-    const int pw = (B + 3) / 4;
-    std::vector<int32_t> w(B + pw + 2 * upd.size());
-    memcpy(w.data(), slots, B * 4);
-    std::vector<uint8_t> pb(pw * 4, 1);
-    if (prot) memcpy(pb.data(), prot, B);
-    memcpy(w.data() + B, pb.data(), pw * 4);
-    for (size_t i = 0; i < upd.size(); ++i) {
-      w[B + pw + 2 * i] = upd[i].first;
-      w[B + pw + 2 * i + 1] = upd[i].second;
-    }
-    if ((r = upload(c, w))) return r;
-    CK(cudaMemcpyAsync(c->slots_d, c->staging_d, B * 4, cudaMemcpyDeviceToDevice, c->st));
-    CK(cudaMemcpyAsync(c->prot_d, c->staging_d + B, B, cudaMemcpyDeviceToDevice, c->st));
-    if (!upd.empty()) {
-      k_apply_pt<<<cdiv((int)upd.size(), 128), 128, 0, c->st>>>(c->pt_d, c->staging_d + B + pw, (int)upd.size());
-      CK(cudaGetLastError());
-      c->launches++;
-    }
-  }
+  if ((r = upload_batch(c, slots, B, prot))) return r;
   // the pending list built at the end of the previous step (device ctrl / last / cu_*);
   // rebuilt here (pending-list gate over this batch) when mg_verify_window or
   // mg_release changed the pending set since
@@ -1066,32 +1072,8 @@ static mg_status decode_fused(mg_ctx* c, const int32_t* slots, int B, const uint
   const int n_list = (int)last.size();
   size_t ev0 = 0;
   if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
-  std::vector<std::pair<int, int>> upd;
-  for (int b = 0; b < B; ++b) {
-    const int s = slots[b];
-    if (c->pos_h[s] / c->PS >= (int)c->pages[s].size()) alloc_page(c, s, &upd);
-  }
-  mg_status r;
-  {
-    const int pw = (B + 3) / 4;
-    std::vector<int32_t> w(B + pw + 2 * upd.size());
-    memcpy(w.data(), slots, B * 4);
-    std::vector<uint8_t> pb(pw * 4, 1);
-    if (prot) memcpy(pb.data(), prot, B);
-    memcpy(w.data() + B, pb.data(), pw * 4);
-    for (size_t i = 0; i < upd.size(); ++i) {
-      w[B + pw + 2 * i] = upd[i].first;
-      w[B + pw + 2 * i + 1] = upd[i].second;
-    }
-    if ((r = upload(c, w))) return r;
-    CK(cudaMemcpyAsync(c->slots_d, c->staging_d, B * 4, cudaMemcpyDeviceToDevice, c->st));
-    CK(cudaMemcpyAsync(c->prot_d, c->staging_d + B, B, cudaMemcpyDeviceToDevice, c->st));
-    if (!upd.empty()) {
-      k_apply_pt<<<cdiv((int)upd.size(), 128), 128, 0, c->st>>>(c->pt_d, c->staging_d + B + pw, (int)upd.size());
-      CK(cudaGetLastError());
-      c->launches++;
-    }
-  }
+  mg_status r = upload_batch(c, slots, B, prot);
+  if (r) return r;
   GateArgs ga{};
   ga.g = c->f_g; ga.prot = c->prot_d; ga.tau = tau; ga.slots = c->slots_d; ga.B = B;
   ga.pos = c->pos_d; ga.shadow_len = c->shadow_d; ga.hist = c->hist_d; ga.hist_stride = c->cfg.max_seq + 1;
@@ -1356,31 +1338,9 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
   if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
 
   // 1. upload batch + page-table updates (one H2D copy)
-  std::vector<std::pair<int, int>> upd;
-  for (int b = 0; b < B; ++b) {
-    const int s = slots[b];
-    if (c->pos_h[s] / c->PS >= (int)c->pages[s].size()) alloc_page(c, s, &upd);
-  }
   {
-    const int pw = (B + 3) / 4;  // prot bytes packed in words
-    std::vector<int32_t> w(B + pw + 2 * upd.size());
-    memcpy(w.data(), slots, B * 4);
-    std::vector<uint8_t> pb(pw * 4, 1);
-    if (prot) memcpy(pb.data(), prot, B);
-    memcpy(w.data() + B, pb.data(), pw * 4);
-    for (size_t i = 0; i < upd.size(); ++i) {
-      w[B + pw + 2 * i] = upd[i].first;
-      w[B + pw + 2 * i + 1] = upd[i].second;
-    }
-    mg_status r = upload(c, w);
+    mg_status r = upload_batch(c, slots, B, prot);
     if (r) return r;
-    CK(cudaMemcpyAsync(c->slots_d, c->staging_d, B * 4, cudaMemcpyDeviceToDevice, c->st));
-    CK(cudaMemcpyAsync(c->prot_d, c->staging_d + B, B, cudaMemcpyDeviceToDevice, c->st));
-    if (!upd.empty()) {
-      k_apply_pt<<<cdiv((int)upd.size(), 128), 128, 0, c->st>>>(c->pt_d, c->staging_d + B + pw, (int)upd.size());
-      CK(cudaGetLastError());
-      c->launches++;
-    }
   }
   // 2. fast path (one CUDA graph per (B, attention splits))
   Sched fs = sched_fast(c, B, max_ctx);
