@@ -481,7 +481,14 @@ def run_gpu(args):
                      "fast_step_ms_timed_pass": round(tim["step_ms"] / max(tim["steps"], 1), 4),
                      # the whole pipelined BF16 step (CUDA graph, PDL) against the same peak:
                      # algorithmic bytes = weights once + every row's K/V context
-                     "step": _step_roofline(shp, B, ctx0 + W + K // 2, T["bf16"] / K, hbm)},
+                     "step": _step_roofline(shp, B, ctx0 + W + K // 2, T["bf16"] / K, hbm),
+                     # the synchronous verifier launches against the same peak --
+                     # time = always-on step - BF16 step; bytes = weights once + the verified
+                     # rows' shadow K/V (one protected row / all rows)
+                     "verifier": {p: _verifier_roofline(shp, n, ctx0 + W + K // 2, (T[a] - T["bf16"]) / K, hbm)
+                                  for p, n, a in (("one", 1, "ao" if args.protected == "one" else "ao_other"),
+                                                  ("all", B, "ao_other" if args.protected == "one" else "ao"))
+                                  if a in T}},
         "e2e": {"value": round(tok / (t_e2e * 1e-3), 2), "unit": "tok/s", "h2d_bytes_per_step": B * 5,
                 "d2h_bytes_per_step": B * 5},
         "gpu_launches": res["mg"]["launches"],
@@ -551,6 +558,14 @@ def _step_roofline(shp, B, ctx, ms, peak_gbs):
     gbs = (w + kv) / (ms * 1e-3) / 1e9
     return {"bytes": w + kv, "weights": w, "kv": kv, "ms": round(ms, 4), "achieved": round(gbs, 1),
             "frac": round(gbs / peak_gbs, 4)}
+
+
+def _verifier_roofline(shp, rows, ctx, ms, peak_gbs):
+    """Verifier launch of a step: weights once + `rows` rows'
+    shadow K/V over `ctx` keys, in `ms` (always-on minus BF16 step time)."""
+    r = _step_roofline(shp, rows, ctx, ms, peak_gbs)
+    r["rows"] = rows
+    return r
 
 
 def _oracle_sample(shp, prompt_len, steps, tau, budget_s):
