@@ -931,6 +931,42 @@ def run_sweep(args):
                              "sweep on calibration prompts, A6000 -- context, not the target"}
 
 
+def run_batch_scaling(args):
+    """tab:batch_scaling analog: latency increment over BF16
+    of MarginGate (tau100 calibrated per batch on seeds 1000 + i) and of
+    always-on verification, synchronous and fused verify modes, one protected
+    request, at batch 8 / 16 / 32 / 64."""
+    from paper_2605_30218_b200 import inputs, metrics
+    from paper_2605_30218_b200.engine import Engine
+
+    shp = inputs.shape(args.model)
+    K, W = args.steps, args.warmup
+    prompt_len, decode_len = inputs.WORKLOADS[args.workload]
+    ctx0 = prompt_len + decode_len // 2 - W
+    rows = []
+    for B in (8, 16, 32, 64):
+        eng = Engine(shp, max_batch=B, max_slots=B, max_seq=ctx0 + W + K + 2, page_size=64)
+        cal = calibrate(eng, inputs.prompts(B, ctx0, shp["vocab"], seed=1000), 3, min(K, 16))
+        t100 = cal["tau100"] if cal["tau100"] is not None else math.inf
+        ev = inputs.prompts(B, ctx0, shp["vocab"], seed=7)
+        p1 = inputs.protected_mask(B, "one")
+        r = {n: _decode_run(eng, ev, t, p1, W, K, timed=True, fused=f)
+             for n, t, f in (("bf16", 0.0, False), ("margingate", t100, False), ("always_on", math.inf, False),
+                             ("margingate_fused", t100, True), ("always_on_fused", math.inf, True))}
+        eng.close()
+        inc = {n: round(metrics.latency_increment(r[n][2], r["bf16"][2]), 4) for n in r if n != "bf16"}
+        rows.append({"batch": B, "tau100": t100, "eps_pert_max": cal["eps_pert_max"],
+                     "bf16_tok_s": round(B * K / (r["bf16"][2] * 1e-3), 2), "inc": inc,
+                     "trigger_pct": round(100 * metrics.rates(r["margingate"][1])["r_verify"], 3),
+                     "protected_row_equals_reference": {n: r[n][0][0] == r["always_on"][0][0]
+                                                        for n in ("bf16", "margingate", "margingate_fused")}})
+    return {"metric": "batch-scaling latency increments (tab:batch_scaling analog)", "model": args.model,
+            "workload": f"{args.workload}-shaped, context {ctx0 + W}..{ctx0 + W + K}, one protected request",
+            "rows": rows,
+            "paper_context": "PAPER.md:331-334 (A6000, 8B): LLM-42 64.6/69.0/73.8/106.5% vs MarginGate "
+                             "29.0/45.4/61.6/73.6% at bs 8/16/32/64 -- context, not the target"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -948,9 +984,13 @@ def main():
     ap.add_argument("--window", type=int, default=64, help="LLM-42 verify window (PAPER.md:251 K=64)")
     ap.add_argument("--sweep", action="store_true", help="tau calibration sweep report (NEXT-1) instead of the "
                                                           "bench line")
+    ap.add_argument("--batch-scaling", action="store_true", help="tab:batch_scaling analog report instead of the "
+                                                                   "bench line")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3"
-    if args.sweep:
+    if args.batch_scaling:
+        line = run_batch_scaling(args)
+    elif args.sweep:
         line = run_sweep(args)
     else:
         line = run_reference(args) if args.impl == "reference" else run_gpu(args)
