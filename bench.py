@@ -898,6 +898,29 @@ def run_sweep(args):
                                                                        [ref_e[i] for i in pr]), 2)
                                 for n in ("bf16", "margingate")},
         }
+    # SURVEY A24 (seq. det. over >= 120 protected sequences):
+    # every row protected, `trials` disjoint evaluation batches (seeds 7 + B j)
+    trials = {"tau": t_eval, "tau_p": cal["tau_p"], "batches": args.trials, "protected_sequences": 0,
+              "deterministic": {"bf16": 0, "margingate": 0, "margingate_tau_p": 0}, "triggers": 0,
+              "triggers_tau_p": 0, "protected_steps": 0}
+    pall = inputs.protected_mask(B, "all")
+    for j in range(args.trials):
+        evj = inputs.prompts(B, prompt_len, shp["vocab"], seed=7 + B * j)
+        ref_j = _decode_run(eng, evj, math.inf, pall, W, K)[0]
+        for n, tau in (("bf16", 0.0), ("margingate", t_eval), ("margingate_tau_p", cal["tau_p"])):
+            sj, stj, _ = _decode_run(eng, evj, tau, pall, W, K)
+            trials["deterministic"][n] += sum(1 for i in range(B) if sj[i] == ref_j[i])
+            if n == "margingate":
+                trials["triggers"] += stj["triggers"]
+                trials["protected_steps"] += stj["protected_rows"]
+            if n == "margingate_tau_p":
+                trials["triggers_tau_p"] += stj["triggers"]
+        trials["protected_sequences"] += B
+    trials["determinism_pct"] = {n: round(100 * v / max(trials["protected_sequences"], 1), 2)
+                                 for n, v in trials["deterministic"].items()}
+    trials["trigger_pct"] = round(100 * trials["triggers"] / max(trials["protected_steps"], 1), 3)
+    trials["trigger_pct_tau_p"] = round(100 * trials["triggers_tau_p"] / max(trials["protected_steps"], 1), 3)
+    evals["trials_all_protected"] = trials
     eng.close()
     # NEXT-3 (App. C tab:hetero): trigger check on same-prompt-replicated
     # (homogeneous) vs mixed prompts of ragged lengths (heterogeneous; per-row
@@ -984,6 +1007,8 @@ def main():
     ap.add_argument("--window", type=int, default=64, help="LLM-42 verify window (PAPER.md:251 K=64)")
     ap.add_argument("--sweep", action="store_true", help="tau calibration sweep report (NEXT-1) instead of the "
                                                           "bench line")
+    ap.add_argument("--trials", type=int, default=15, help="--sweep: evaluation batches (B x trials protected "
+                                                          "sequences, SURVEY A24)")
     ap.add_argument("--batch-scaling", action="store_true", help="tab:batch_scaling analog report instead of the "
                                                                    "bench line")
     args = ap.parse_args()
