@@ -42,6 +42,13 @@ mg_status mgd_gemm(const uint16_t* x, const uint16_t* W, int32_t T, int32_t N, i
 
 /* QKV epilogue: acc = sum_s part[s][t][:] (+bias) -> RoPE(q,k) -> q[T][H*hd],
  * k[T][KV*hd], v[T][KV*hd] (dense outputs, not the paged cache). */
+/* LM head with the FUSED top-1/top-2 epilogue (the engine's path):
+ * tcgen05 GEMM of x [T][K] by W [N][K] (row-major bf16; N % 128 == 0) whose
+ * epilogue writes one top-2 set per (token, 128-row tile), then the tile merge;
+ * outputs per token v1, i1, v2, i2, g = v1 - v2 (device), *nan_flag |= 1 on a
+ * NaN product sum (ranked -inf).  tile_n 0: the engine's choice. */
+mg_status mgd_gemm_top2(const uint16_t* x, const uint16_t* W, int32_t T, int32_t N, int32_t K, int32_t tile_n,
+                        float* v1, int32_t* i1, float* v2, int32_t* i2, float* g, int32_t* nan_flag, void* stream);
 mg_status mgd_qkv_epilogue(const float* part, int32_t splits, const uint16_t* bias, const int32_t* pos,
                            int32_t T, int32_t H, int32_t KV, int32_t hd, float theta, int32_t max_pos,
                            uint16_t* q, uint16_t* k, uint16_t* v, void* stream);

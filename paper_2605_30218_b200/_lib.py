@@ -59,7 +59,7 @@ DEBUG_SYMBOLS = ["mgd_gen_tensor", "mgd_rmsnorm", "mgd_gemm", "mgd_qkv_epilogue"
                  "mgd_swiglu", "mgd_top2", "mgd_gate", "mgd_read_column", "mgd_cache_digest", "mgd_last_step",
                  "mgd_capture_logits", "mgd_weight", "mgd_schedule", "mgd_launch_count", "mgd_set_timing",
                  "mgd_timing", "mgd_chain_trace", "mgd_capture_verifier_logits", "mgd_set_inject",
-                 "mgd_force_schedule"]
+                 "mgd_force_schedule", "mgd_gemm_top2"]
 
 _vp, _i32, _u32, _i64, _u64, _f32 = C.c_void_p, C.c_int32, C.c_uint32, C.c_int64, C.c_uint64, C.c_float
 _P = C.POINTER
@@ -72,6 +72,7 @@ _SIGS = {
     "mg_stats": [_vp, _P(MgStats)],
     "mg_set_policy": [_vp, _i32, _i32, _i32],
     "mgd_set_inject": [_vp, _f32, _u64],
+    "mgd_gemm_top2": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "mgd_force_schedule": [_vp, _i32],
     "mg_verify_window": [_vp, _vp, _i32, _vp, _vp, _vp],
     "mg_release": [_vp, _i32],

@@ -67,6 +67,36 @@ mg_status mgd_gemm(const uint16_t* x, const uint16_t* W, int32_t T, int32_t N, i
   return st_of(e);
 }
 
+mg_status mgd_gemm_top2(const uint16_t* x, const uint16_t* W, int32_t T, int32_t N, int32_t K, int32_t tile_n,
+                        float* v1, int32_t* i1, float* v2, int32_t* i2, float* g, int32_t* nan_flag, void* stream) {
+  if (!x || !W || !v1 || !i1 || !v2 || !i2 || !g || !nan_flag || T < 1 || N % 128 || K % 64) return MG_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (tile_n <= 0) tile_n = gemm_tile_n(T);
+  std::vector<uint16_t> rm((size_t)N * K), tl((size_t)N * K);
+  cudaStreamSynchronize(st);
+  if (cudaMemcpy(rm.data(), W, rm.size() * 2, cudaMemcpyDeviceToHost) != cudaSuccess) return MG_ERR_CUDA;
+  for (size_t r = 0; r < (size_t)N; ++r)
+    for (size_t k = 0; k < (size_t)K; ++k) tl[tiled_offset(r, k, K)] = rm[r * K + k];
+  uint16_t* Wt = nullptr;
+  float* t2 = nullptr;
+  if (cudaMalloc(&Wt, tl.size() * 2) != cudaSuccess) return MG_ERR_CUDA;
+  if (cudaMalloc(&t2, (size_t)T * (N / 128) * 16) != cudaSuccess) {
+    cudaFree(Wt);
+    return MG_ERR_CUDA;
+  }
+  cudaMemcpy(Wt, tl.data(), tl.size() * 2, cudaMemcpyHostToDevice);
+  CUtensorMap mw, mx;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (make_tmap_w_tiled(&mw, Wt, K, N) && make_tmap_2d(&mx, x, K, T, tile_n)) {
+    e = launch_gemm_tc(mw, mx, N, K, T, 1, 0, tile_n, tile_n, nullptr, st, t2, nan_flag);
+    if (e == cudaSuccess) e = launch_top2_tiles(t2, T, N / 128, v1, i1, v2, i2, g, st);
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(Wt);
+  cudaFree(t2);
+  return st_of(e);
+}
+
 mg_status mgd_qkv_epilogue(const float* part, int32_t splits, const uint16_t* bias, const int32_t* pos, int32_t T,
                            int32_t H, int32_t KV, int32_t hd, float theta, int32_t max_pos, uint16_t* q, uint16_t* k,
                            uint16_t* v, void* stream) {

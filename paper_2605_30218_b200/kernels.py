@@ -145,6 +145,23 @@ def top2(logits: np.ndarray):
                 g=g.cpu().numpy(), nan=bool(nan.item()))
 
 
+def gemm_top2(x: np.ndarray, W: np.ndarray, tile_n=0):
+    """LM head with the fused top-2 epilogue (include/mg_debug.h mgd_gemm_top2)."""
+    torch = _t()
+    T, K = x.shape
+    N = W.shape[0]
+    xd, wd = to_dev_u16(x), to_dev_u16(W)
+    f = lambda dt: torch.empty(T, dtype=dt, device="cuda")
+    v1, v2, g = f(torch.float32), f(torch.float32), f(torch.float32)
+    i1, i2 = f(torch.int32), f(torch.int32)
+    nan = torch.zeros(1, dtype=torch.int32, device="cuda")
+    check(lib().mgd_gemm_top2(_p(xd), _p(wd), T, N, K, tile_n, _p(v1), _p(i1), _p(v2), _p(i2), _p(g), _p(nan),
+                              _stream()), None, "gemm_top2")
+    _sync()
+    return dict(v1=v1.cpu().numpy(), i1=i1.cpu().numpy(), v2=v2.cpu().numpy(), i2=i2.cpu().numpy(),
+                g=g.cpu().numpy(), nan=bool(nan.item()))
+
+
 def gate(g: np.ndarray, prot: np.ndarray, tau: float):
     torch = _t()
     B = g.size

@@ -262,3 +262,28 @@ def test_gate_exact(orc, K):
             ref = orc.gate(g, prot, tau)
             assert np.array_equal(rows, ref)
             assert np.array_equal(np.nonzero(trig)[0], ref)
+
+
+@pytest.mark.parametrize("T,tile", [(5, 16), (64, 64), (70, 80)])
+def test_fused_lm_top2_epilogue(orc, K, T, tile):
+    """The LM head's fused top-2 epilogue (mgd_gemm_top2) equals the oracle's
+    top-2 (value desc, id asc; NaN as -inf + flag) applied
+    to the same tcgen05 GEMM's fp32 logits -- bit for bit, including a tie
+    between two rows in different 128-row tiles (lowest id wins, g = 0) and a
+    NaN weight row."""
+    rng = np.random.default_rng(T * 7 + tile)
+    N, K_ = 640, 256
+    x = _rand(orc, rng, (T, K_))
+    W = _rand(orc, rng, (N, K_), 1 / np.sqrt(K_))
+    xf = (x.astype(np.uint32) << 16).view(np.float32)
+    row = np.where(xf[0] >= 0, 0x3F00, 0xBF00).astype(np.uint16)   # +-0.5: row . x[0] = 0.5 sum|x0| (maximal)
+    W[130] = row
+    W[600] = row                                                    # exact tie across tiles 1 and 4
+    W[7, 3] = 0x7FC0                                                # NaN weight -> NaN logit in every token
+    got = K.gemm_top2(x, W, tile_n=tile)
+    logits = K.gemm(x, W, splits=1, impl=0, tile_n=tile)[0]
+    ref = orc.top2(logits)
+    for k in ("v1", "i1", "v2", "i2", "g"):
+        assert np.array_equal(got[k], ref[k]), k
+    assert got["nan"] and ref["nan"]
+    assert got["i1"][0] == 130 and got["i2"][0] == 600 and got["g"][0] == 0.0
