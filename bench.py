@@ -323,6 +323,16 @@ def run_gpu(args):
         ew.close()
         eng = None
 
+    # the whole MATH500-shaped decode at this batch (contexts 131..640 cross the
+    # verifier's 512-key split): MarginGate's triggers, determinism and cost
+    # where the fast path really differs from the verifier (rank-local)
+    full = None
+    if not args.quick and args.full_decode_arm:
+        if eng is not None:
+            eng.close()
+            eng = None
+        full = run_full_decode(args, pnames=("one",))
+
     paper = None
     if not args.quick and args.paper_batch > 0:
         if eng is not None:
@@ -438,6 +448,10 @@ def run_gpu(args):
         "determinism_pct": round(100 * df[0] / df[1], 2) if df[1] else None,
         "note": "MG_VERIFY_FUSED: every protected row's verifier token computed speculatively in the same "
                 "weight pass; the gate selects which to commit (synchronous semantics)"}
+    if full is not None:
+        arms_out["full_decode"] = {"workload": full["workload"], "calibration": full["calibration"],
+                                   **full["arms"]["one"], "protected": "one",
+                                   "note": "rank 0; the whole decode, tau100 calibrated over the same length"}
     if w64 is not None:
         arms_out["llm42_window"] = {
             p: {"window": args.window, "steps": 2 * args.window, "tok_s": round(v[1] / (v[2] * 1e-3), 2),
@@ -954,6 +968,52 @@ def run_sweep(args):
                              "sweep on calibration prompts, A6000 -- context, not the target"}
 
 
+def run_full_decode(args, pnames=("one", "all"), eng=None):
+    """The whole MATH500-shaped decode at the headline batch (prompt 128, all
+    512 decode steps, SURVEY 8(d) "tok/s = emitted decode tokens / decode time"):
+    contexts 128..640 cross the verifier's 512-key split, so the fast path's
+    batch-shaped attention differs from the verifier in the second half.  tau100
+    calibrated over the same decode length on seeds 1000 + i; arms BF16,
+    MarginGate and always-on, synchronous and fused, one and all rows protected."""
+    from paper_2605_30218_b200 import inputs, metrics
+    from paper_2605_30218_b200.engine import Engine
+
+    shp = inputs.shape(args.model)
+    B, W = args.batch, 3
+    prompt_len, decode_len = inputs.WORKLOADS[args.workload]
+    K = decode_len - W
+    own = eng is None
+    if own:
+        eng = Engine(shp, max_batch=B, max_slots=B, max_seq=prompt_len + decode_len + 2, page_size=64)
+    cal = calibrate(eng, inputs.prompts(B, prompt_len, shp["vocab"], seed=1000), W, K)
+    t100 = cal["tau100"] if cal["tau100"] is not None else math.inf
+    ev = inputs.prompts(B, prompt_len, shp["vocab"], seed=7)
+    out = {}
+    for pname in pnames:
+        prot = inputs.protected_mask(B, pname)
+        r = {n: _decode_run(eng, ev, t, prot, W, K, timed=True, fused=f)
+             for n, t, f in (("bf16", 0.0, False), ("margingate", t100, False), ("always_on", math.inf, False),
+                             ("margingate_fused", t100, True), ("always_on_fused", math.inf, True))}
+        pr = [i for i in range(B) if prot[i]]
+        ref = r["always_on"][0]
+        out[pname] = {
+            "tok_s": {n: round(B * K / (v[2] * 1e-3), 2) for n, v in r.items()},
+            "inc": {n: round(metrics.latency_increment(v[2], r["bf16"][2]), 4) for n, v in r.items() if n != "bf16"},
+            "trigger_pct": round(100 * metrics.rates(r["margingate"][1])["r_verify"], 3),
+            "determinism_pct": {n: round(100 * metrics.seq_determinism([r[n][0][i] for i in pr],
+                                                                       [ref[i] for i in pr]), 2)
+                                for n in ("bf16", "margingate", "margingate_fused")}}
+        inc_mg, inc_ao = out[pname]["inc"]["margingate"], out[pname]["inc"]["always_on"]
+        out[pname]["increment_ratio"] = round(metrics.increment_ratio(inc_ao, inc_mg), 3) if inc_mg > 0.01 else None
+    if own:
+        eng.close()
+    return {"metric": "full-decode tok/s, increments, triggers, determinism", "model": args.model,
+            "workload": f"{args.workload}-shaped prompt {prompt_len}, {K} timed decode steps after {W} "
+                        f"(contexts {prompt_len + W}..{prompt_len + decode_len}), batch {B}",
+            "calibration": {k: cal[k] for k in ("eps_pert_max", "tau_p", "tau100", "sync_flip_rate", "flip_events")},
+            "arms": out}
+
+
 def run_batch_scaling(args):
     """tab:batch_scaling analog: latency increment over BF16
     of MarginGate (tau100 calibrated per batch on seeds 1000 + i) and of
@@ -1009,11 +1069,17 @@ def main():
                                                           "bench line")
     ap.add_argument("--trials", type=int, default=15, help="--sweep: evaluation batches (B x trials protected "
                                                           "sequences, SURVEY A24)")
+    ap.add_argument("--no-full-decode-arm", dest="full_decode_arm", action="store_false",
+                    help="skip the whole-decode arm of the bench line")
+    ap.add_argument("--full-decode", action="store_true", help="whole-decode report (all decode steps) instead "
+                                                                 "of the bench line")
     ap.add_argument("--batch-scaling", action="store_true", help="tab:batch_scaling analog report instead of the "
                                                                    "bench line")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3"
-    if args.batch_scaling:
+    if args.full_decode:
+        line = run_full_decode(args)
+    elif args.batch_scaling:
         line = run_batch_scaling(args)
     elif args.sweep:
         line = run_sweep(args)
