@@ -351,11 +351,19 @@ void or_top2(const float* logits, int32_t T, int32_t V, float* v1, int32_t* i1, 
 }
 
 /* Threshold trigger, PAPER.md:201 ("triggers the verifier when g < tau"),
- * protected requests only; rows in ascending order. */
+ * protected requests only; rows in ascending order.
+ * DESIGN.md A4/A7: tau = 0 never fires (pure BF16, r_verify = 0) and
+ * tau = +inf always fires (always-on, r_verify = 1) -- also for
+ * a margin of +inf (second logit -inf); a NaN margin (every logit NaN, ranked
+ * -inf) fires for any tau > 0. */
+static int gate_fires(float g, float tau) {
+  return tau > 0.0f && (g < tau || isinf(tau) || g != g);
+}
+
 int32_t or_gate(const float* g, const uint8_t* prot, int32_t B, float tau, int32_t* rows_out) {
   int32_t n = 0;
   for (int32_t b = 0; b < B; ++b)
-    if (prot[b] && g[b] < tau) rows_out[n++] = b;
+    if (prot[b] && gate_fires(g[b], tau)) rows_out[n++] = b;
   return n;
 }
 
@@ -597,7 +605,7 @@ int32_t or_step(or_state* s, const int32_t* rows, int32_t B, const uint8_t* prot
   /* (2) gate + compaction. */
   int32_t n_trig = 0;
   for (int32_t b = 0; b < B; ++b) {
-    tr[b] = forced_trig ? forced_trig[b] : (uint8_t)(prot[b] && gg[b] < tau);
+    tr[b] = forced_trig ? forced_trig[b] : (uint8_t)(prot[b] && gate_fires(gg[b], tau));
     n_trig += tr[b];
     if (trig) trig[b] = tr[b];
   }

@@ -113,6 +113,11 @@ cudaError_t launch_top2_tiles(const float* t2, int T, int nt, float* v1, int32_t
 }
 
 // ------------------------------------------------------------------ gate
+// The trigger g < tau, strict, with DESIGN.md A4/A7 for the
+// non-finite cases: tau = +inf fires for every margin (always-on, r_verify = 1,
+// PAPER.md:215), a NaN margin (all logits NaN) fires for any tau > 0.
+MG_DEV bool gate_fires(float g, float tau) { return tau > 0.f && (g < tau || isinf(tau) || g != g); }
+
 // Single CTA of 1024 threads (B <= 1024).  Row b = thread b.
 __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
   griddep();
@@ -132,7 +137,7 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
       tr = a.prot ? a.prot[b] != 0 : true;
     } else {
       const bool prot = a.prot ? a.prot[b] != 0 : true;
-      tr = prot && (a.g[b] < a.tau);  // strict <
+      tr = prot && gate_fires(a.g[b], a.tau);  // strict <
     }
   }
   const int gap = tr ? (p - s0 + 1) : 0;
@@ -243,7 +248,7 @@ __global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
   const int slot = a.slots[b];
   const int p = a.pos[slot];
   const bool listed = a.gate_ran && a.trig[b];
-  const bool tr = listed && (!a.spec || a.g[b] < a.spec_tau);  // fused mode: the gate, strict <
+  const bool tr = listed && (!a.spec || gate_fires(a.g[b], a.spec_tau));  // fused mode: the gate
   const int f = a.f_tok[b];
   const int v = tr ? a.v_tok[a.rank[b]] : -1;
   const int kind = !tr ? 0 : (v == f ? 1 : 2);
@@ -373,7 +378,10 @@ __global__ void __launch_bounds__(256) k_commit_fused(FusedCommitArgs a) {
   const bool prot = a.prot ? a.prot[b] != 0 : true;
   unsigned long long* s = a.stats;
   atomicAdd(&s[1], 1ull);
-  if (prot) atomicAdd(&s[2], 1ull);
+  // a replacement step (kind 4) drops the row's fast output: no gate decision,
+  // so it is not a protected row of r_verify's denominator (r_verify = 1 at
+  // tau = +inf, as in the synchronous mode)
+  if (prot && !rep) atomicAdd(&s[2], 1ull);
   if (pend) atomicAdd(&s[rep ? 5 : 4], 1ull);
   if (b == 0) {
     atomicAdd(&s[0], 1ull);
@@ -392,7 +400,7 @@ __global__ void __launch_bounds__(256) k_commit_fused(FusedCommitArgs a) {
     out = v;
   } else {
     out = a.f_tok[b];
-    gated = a.gate_on && prot && a.g[b] < a.tau;  // strict <
+    gated = a.gate_on && prot && gate_fires(a.g[b], a.tau);  // strict <
     h[p + 1] = out;
     a.pos[slot] = p + 1;
     a.pend[slot] = gated ? 1 : 0;

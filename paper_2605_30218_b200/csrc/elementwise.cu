@@ -210,19 +210,82 @@ cudaError_t launch_epi_residual(const uint16_t* x, const float* part, PartSpec p
 
 // ------------------------------------------------------------------ a6: SwiGLU
 // thread per 4 consecutive outputs (epilogue.cuh swiglu4)
+// The kernel is L2-latency bound: its time is the number of rounds of partial
+// loads.  With the slot count of the op's partition known at launch (<= 2 for
+// the stream-K gate/up GEMMs of the model shapes), the light SMAX = 2 form
+// keeps the registers low enough that every item's loads are in flight in one
+// wave of threads.
+template <int SMAX>
 __global__ void k_epi_swiglu(const float* __restrict__ part, PartSpec ps, int T, int F, uint16_t* __restrict__ out) {
   griddep();
   const size_t n4 = (size_t)T * F / 4;
   for (size_t e4 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e4 < n4; e4 += (size_t)gridDim.x * blockDim.x)
-    swiglu4(part, ps, T, F, e4 * 4, out);
+    swiglu4_s<SMAX>(part, ps, T, F, e4 * 4, out);
 }
 
+// two items per thread, every load of both issued before any arithmetic, for
+// partitions with <= 2 slots per output (one round of L2 latency per thread)
+__global__ void __launch_bounds__(256) k_epi_swiglu2(const float* __restrict__ part, PartSpec ps, int T, int F,
+                                                     uint16_t* __restrict__ out) {
+  griddep();
+  const size_t n4 = (size_t)T * F / 4;
+  const size_t stride = (size_t)T * 2 * F;
+  const size_t nth = (size_t)gridDim.x * blockDim.x;
+  const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float4 v[2][4];
+  size_t e[2];
+  int S[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const size_t e4 = i0 + k * nth;
+    e[k] = e4 * 4;
+    S[k] = 0;
+    if (e4 < n4) {
+      const int t = (int)e[k] / F, j = (int)e[k] % F;
+      const int col = (j / 64) * 128 + (j % 64);
+      S[k] = part_count(ps, col);
+      const float* p0 = part + (size_t)t * 2 * F + (size_t)col;
+      v[k][0] = __ldcg(reinterpret_cast<const float4*>(p0));
+      v[k][1] = __ldcg(reinterpret_cast<const float4*>(p0 + 64));
+      if (S[k] > 1) {
+        v[k][2] = __ldcg(reinterpret_cast<const float4*>(p0 + stride));
+        v[k][3] = __ldcg(reinterpret_cast<const float4*>(p0 + stride + 64));
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (S[k] == 0) continue;
+    float4 g = v[k][0], u = v[k][1];
+    if (S[k] > 1) {
+      g.x = __fadd_rn(g.x, v[k][2].x); g.y = __fadd_rn(g.y, v[k][2].y); g.z = __fadd_rn(g.z, v[k][2].z); g.w = __fadd_rn(g.w, v[k][2].w);
+      u.x = __fadd_rn(u.x, v[k][3].x); u.y = __fadd_rn(u.y, v[k][3].y); u.z = __fadd_rn(u.z, v[k][3].z); u.w = __fadd_rn(u.w, v[k][3].w);
+    }
+    const float gg[4] = {g.x, g.y, g.z, g.w}, uu[4] = {u.x, u.y, u.z, u.w};
+    float a[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) a[q] = __fmul_rn(__fdiv_rn(gg[q], __fadd_rn(1.0f, expf(-gg[q]))), uu[q]);
+    *reinterpret_cast<uint2*>(out + e[k]) = make_uint2(pack_bf2(a[0], a[1]), pack_bf2(a[2], a[3]));
+  }
+}
+
+#ifndef MG_SWIGLU_LIGHT
+#define MG_SWIGLU_LIGHT 2
+#endif
 cudaError_t launch_epi_swiglu(const float* part, PartSpec ps, int T, int F, uint16_t* out, cudaStream_t st) {
   if ((long long)T * 2 * F >= (1LL << 31)) return cudaErrorInvalidValue;
   const size_t n4 = (size_t)T * F / 4;
   size_t blocks = (n4 + 255) / 256;
+  if (MG_SWIGLU_LIGHT == 2 && part_slots(ps, 2 * F) <= 2) {
+    const size_t b2 = (n4 + 511) / 512;
+    return launch_k(k_epi_swiglu2, dim3((unsigned)b2), dim3(256), 0, st, part, ps, T, F, out);
+  }
+  if (MG_SWIGLU_LIGHT && part_slots(ps, 2 * F) <= 2) {
+    if (blocks > (size_t)num_sms() * 64) blocks = (size_t)num_sms() * 64;
+    return launch_k(k_epi_swiglu<2>, dim3((unsigned)blocks), dim3(256), 0, st, part, ps, T, F, out);
+  }
   if (blocks > 148 * 16) blocks = 148 * 16;
-  return launch_k(k_epi_swiglu, dim3((unsigned)blocks), dim3(256), 0, st, part, ps, T, F, out);
+  return launch_k(k_epi_swiglu<4>, dim3((unsigned)blocks), dim3(256), 0, st, part, ps, T, F, out);
 }
 
 // ------------------------------------------------------------------ row gather

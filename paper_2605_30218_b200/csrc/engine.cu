@@ -871,6 +871,14 @@ static mg_status pipe_refresh(mg_ctx* c) {
   return MG_OK;
 }
 
+// the pipelined mode's next step reuses the device pending list built by the
+// previous step's gate; anything that overwrites cu_* / last_d while slots are
+// pending (prefill, window verification) must make it rebuild the list
+static void mark_pending_list_dirty(mg_ctx* c) {
+  for (int s = 0; s < c->cfg.max_slots; ++s)
+    if (c->active[s] && c->pend_h[s]) c->pend_dirty = true;
+}
+
 static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const uint8_t* prot, float tau,
                                   int32_t* tokens_out, uint8_t* kind_out, float* margin_out) {
   mg_status r = pipe_refresh(c);
@@ -1303,6 +1311,9 @@ mg_status mg_prefill(mg_ctx* c, int32_t slot, const int32_t* prompt, int32_t len
   c->launches += 2;
   CK(cudaMemcpyAsync(first_token, c->v_tok, 4, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  // the prefill overwrote the device catch-up list (cu_*, last_d) that the
+  // pipelined mode's next step would reuse for the pending slots: rebuild it
+  mark_pending_list_dirty(c);
   c->pos_h[slot] = len;
   c->shadow_h[slot] = len;
   c->active[slot] = 1;
@@ -1344,7 +1355,11 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
   }
   // 2. fast path (one CUDA graph per (B, attention splits))
   Sched fs = sched_fast(c, B, max_ctx);
-  mg_status r = graphed(c, std::make_tuple(0, B, fs.attn_ns, fs.attn_sk, 0, 0), [&]() -> mg_status {
+  // key: everything the captured launch sequence depends on (schedule mode,
+  // GEMM engine and MMA width, attention splits)
+  mg_status r = graphed(c, std::make_tuple(0, B, fs.attn_ns, fs.attn_sk, c->fast_mode,
+                                           fs.qkv.impl * 4096 + fs.qkv.mma_n * 8 + (c->lm_unfused ? 1 : 0)),
+                        [&]() -> mg_status {
     CK(launch_prepare(c->slots_d, B, c->pos_d, c->hist_d, c->cfg.max_seq + 1, c->f_slot, c->f_pos, c->f_tok,
                       c->f_nk, c->st));
     c->launches++;
@@ -1495,6 +1510,9 @@ mg_status mg_verify_window(mg_ctx* c, const int32_t* slots, int32_t n, int32_t* 
     CK(cudaStreamSynchronize(c->st));
     memcpy(res.data() + i0, res_h, (size_t)k * 4);
   }
+  // the window's catch-up list overwrote cu_* / the pending set changed: the
+  // pipelined mode rebuilds its pending list before the next step
+  if (M > 0) mark_pending_list_dirty(c);
   for (int i = 0; i < n; ++i) {
     const int s = slots[i];
     c->pos_h[s] = res[3 * i];

@@ -92,6 +92,48 @@ __device__ __forceinline__ uint16_t* cache_ptr(const CacheView& c, int slot, int
 
 // ---- SwiGLU: 4 consecutive outputs e..e+3 of a [T][F] (same 64-block, so the
 // gate/up columns are contiguous float4s in the 64-interleaved [gate;up] tile)
+// SMAX: slots whose loads are issued together (more slots are added in a
+// loop, still in slot order); the kernel picks the smallest SMAX covering the
+// op's partition so the thread stays light enough for one wave of threads.
+template <int SMAX>
+__device__ __forceinline__ void swiglu4_s(const float* __restrict__ part, const PartSpec& ps, int T, int F, size_t e,
+                                          uint16_t* __restrict__ out) {
+  const size_t stride = (size_t)T * 2 * F;
+  const int t = (int)e / F;
+  const int j = (int)e % F;
+  const int col = (j / 64) * 128 + (j % 64);
+  const int S = part_count(ps, col);
+  const size_t gcol = (size_t)t * 2 * F + (size_t)col;
+  float4 gs[SMAX], us[SMAX];
+#pragma unroll
+  for (int s = 0; s < SMAX; ++s)
+    if (s < S) {
+      gs[s] = __ldcg(reinterpret_cast<const float4*>(part + (size_t)s * stride + gcol));
+      us[s] = __ldcg(reinterpret_cast<const float4*>(part + (size_t)s * stride + gcol + 64));
+    }
+  float4 g = gs[0], u = us[0];
+#pragma unroll
+  for (int s = 1; s < SMAX; ++s)
+    if (s < S) {
+      g.x = __fadd_rn(g.x, gs[s].x); g.y = __fadd_rn(g.y, gs[s].y); g.z = __fadd_rn(g.z, gs[s].z); g.w = __fadd_rn(g.w, gs[s].w);
+      u.x = __fadd_rn(u.x, us[s].x); u.y = __fadd_rn(u.y, us[s].y); u.z = __fadd_rn(u.z, us[s].z); u.w = __fadd_rn(u.w, us[s].w);
+    }
+  for (int s = SMAX; s < S; ++s) {
+    const float4 g2 = __ldcg(reinterpret_cast<const float4*>(part + (size_t)s * stride + gcol));
+    const float4 u2 = __ldcg(reinterpret_cast<const float4*>(part + (size_t)s * stride + gcol + 64));
+    g.x = __fadd_rn(g.x, g2.x); g.y = __fadd_rn(g.y, g2.y); g.z = __fadd_rn(g.z, g2.z); g.w = __fadd_rn(g.w, g2.w);
+    u.x = __fadd_rn(u.x, u2.x); u.y = __fadd_rn(u.y, u2.y); u.z = __fadd_rn(u.z, u2.z); u.w = __fadd_rn(u.w, u2.w);
+  }
+  const float gg[4] = {g.x, g.y, g.z, g.w}, uu[4] = {u.x, u.y, u.z, u.w};
+  float a[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float den = __fadd_rn(1.0f, expf(-gg[k]));
+    a[k] = __fmul_rn(__fdiv_rn(gg[k], den), uu[k]);
+  }
+  *reinterpret_cast<uint2*>(out + e) = make_uint2(pack_bf2(a[0], a[1]), pack_bf2(a[2], a[3]));
+}
+
 __device__ __forceinline__ void swiglu4(const float* __restrict__ part, const PartSpec& ps, int T, int F, size_t e,
                                         uint16_t* __restrict__ out) {
   const size_t stride = (size_t)T * 2 * F;

@@ -520,3 +520,45 @@ def test_changing_protection_mask_matches_sync(torch, tiny, mode):
         assert n >= steps // 2 and runs[0][b][:n] == runs[1][b][:n], b
     if mode == 2:
         assert runs[0] == runs[1]
+
+
+def test_pipelined_prefill_while_pending(torch, tiny):
+    """a prefill into a never-used slot while other slots hold
+    pending tentative tokens (no mg_verify_window in between) overwrites the
+    device catch-up list the pipelined mode reuses; the next step must rebuild
+    it.  At tau=inf every request's resolved sequence equals its batch-1
+    reference and no false kind-4 replacement appears."""
+    from paper_2605_30218_b200.engine import VERIFY_PIPELINED
+    shp, _ = tiny
+    S, steps = 6, 18
+    reqs = inputs.prompts(S, inputs.ragged_lengths(S, 6, 20, seed=73), shp["vocab"], seed=420)
+    eng = _engine(shp, S)
+    eng.set_policy(verify_mode=VERIFY_PIPELINED)
+    out = torch.empty(S, dtype=torch.int32, device="cuda")
+    kind = torch.empty(S, dtype=torch.uint8, device="cuda")
+    seqs = {s: [eng.prefill(s, reqs[s])] for s in range(4)}
+    for step in range(steps):
+        if step in (5, 11):                       # join while slots 0..3 (and later 4) are pending
+            s = 4 if step == 5 else 5
+            seqs[s] = [eng.prefill(s, reqs[s])]
+        slots = sorted(seqs)
+        eng.step(slots, None, INF, out[:len(slots)], kind[:len(slots)])
+        o, k = out.cpu().numpy(), kind.cpu().numpy()
+        for j, s in enumerate(slots):
+            if k[j] == 4:
+                seqs[s][-1] = int(o[j])
+            else:
+                seqs[s].append(int(o[j]))
+    slots = sorted(seqs)
+    pos, last, _ = eng.verify_window(slots)
+    st = eng.stats()
+    eng.close()
+    for j, s in enumerate(slots):
+        n = int(pos[j]) - len(reqs[s]) + 1
+        seq = seqs[s][:n - 1] + [int(last[j])]
+        e1 = _engine(shp, 1)
+        ref = _decode(torch, e1, [reqs[s]], len(seq), INF)[0]
+        e1.close()
+        assert seq == ref, s
+    # tau = inf: every decision of a protected row triggers (r_verify = 1)
+    assert st["triggers"] == st["protected_rows"]

@@ -351,3 +351,22 @@ def test_gate_special_cases_and_monotone(orc):
     # ascending order
     r = orc.gate(g, np.ones(64, np.uint8), 10.0)
     assert np.all(np.diff(r) > 0)
+
+
+def test_gate_non_finite_margins(orc):
+    """DESIGN.md A4/A7: tau=+inf is always-on for EVERY protected row, also one
+    whose margin is +inf (second logit -inf) -- r_verify = 1 (PAPER.md:215);
+    a row whose logits are all NaN (ranked -inf, A7) has margin -inf - -inf =
+    NaN and fires for any tau > 0; tau = 0 never fires (pure BF16)."""
+    L = np.zeros((4, 8), np.float32)
+    L[0, 3] = 1.0                       # ordinary row: g = 1
+    L[1, :] = -np.inf
+    L[1, 2] = 0.5                       # second logit -inf: g = +inf
+    L[2, :] = np.nan                    # all NaN: v1 = v2 = -inf, g = NaN
+    L[3, 5] = 2.0                       # g = 2
+    g = orc.top2(L)["g"]
+    assert g[0] == 1.0 and np.isposinf(g[1]) and np.isnan(g[2]) and g[3] == 2.0
+    prot = np.array([1, 1, 1, 0], np.uint8)
+    assert orc.gate(g, prot, float("inf")).tolist() == [0, 1, 2]     # always-on: every protected row
+    assert orc.gate(g, prot, 1.5).tolist() == [0, 2]                 # NaN margin fires, +inf does not
+    assert orc.gate(g, prot, 0.0).tolist() == []                     # tau = 0: pure BF16
