@@ -5,7 +5,7 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr \
              -Xptxas -v -Iinclude
 CSRC      := paper_2605_30218_b200/csrc
-SRCS      := $(CSRC)/gemm.cu $(CSRC)/chain.cu $(CSRC)/elementwise.cu $(CSRC)/attention.cu $(CSRC)/control.cu $(CSRC)/engine.cu \
+SRCS      := $(CSRC)/gemm.cu $(CSRC)/elementwise.cu $(CSRC)/attention.cu $(CSRC)/control.cu $(CSRC)/engine.cu \
              $(CSRC)/capi_debug.cu
 BUILD     := build
 OBJS      := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(SRCS))

@@ -28,7 +28,7 @@ mg_status mgd_rmsnorm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t d
                       void* stream);
 
 /* GEMM partials: out[s][t][n] = sum_{k in piece s of n's tile} x[t][k] * W[n][k].
- * impl 0 = tcgen05 (TMA + TMEM), 1 = CUDA-core small-T kernel.
+ * impl must be 0 (tcgen05, TMA + TMEM; other values: MG_ERR_INVALID).
  * splits > 0: uniform split-K count over 64-wide k-blocks (piece s = split s);
  * splits < 0: stream-K over G = -splits virtual CTAs: CTA i owns k-blocks
  * [i W / G, (i+1) W / G) of the W = (N/128)(K/64) tile-major k-blocks, and
@@ -122,12 +122,6 @@ mg_status mgd_launch_count(mg_ctx* ctx, uint64_t* out_host);
  * average ms per launch of the GEMM class and the whole step. */
 mg_status mgd_set_timing(mg_ctx* ctx, int32_t on);
 mg_status mgd_timing(mg_ctx* ctx, double* out8_host);
-
-/* Diagnostics of the persistent layer chain: from the next step on, the chain
- * launch of `layer` records per-CTA globaltimer stamps (chain.h
- * kChainTraceWords per CTA).  *words receives the buffer length; out_host
- * (nullable) receives the stamps of the last traced launch.  layer -2: off. */
-mg_status mgd_chain_trace(mg_ctx* ctx, int32_t layer, unsigned long long* out_host, int32_t* words);
 
 #ifdef __cplusplus
 }

@@ -58,7 +58,7 @@ PUBLIC_SYMBOLS = ["mg_query_sizes", "mg_init", "mg_prefill", "mg_decode_step", "
 DEBUG_SYMBOLS = ["mgd_gen_tensor", "mgd_rmsnorm", "mgd_gemm", "mgd_qkv_epilogue", "mgd_attention", "mgd_residual",
                  "mgd_swiglu", "mgd_top2", "mgd_gate", "mgd_read_column", "mgd_cache_digest", "mgd_last_step",
                  "mgd_capture_logits", "mgd_weight", "mgd_schedule", "mgd_launch_count", "mgd_set_timing",
-                 "mgd_timing", "mgd_chain_trace", "mgd_capture_verifier_logits", "mgd_set_inject",
+                 "mgd_timing", "mgd_capture_verifier_logits", "mgd_set_inject",
                  "mgd_force_schedule", "mgd_gemm_top2"]
 
 _vp, _i32, _u32, _i64, _u64, _f32 = C.c_void_p, C.c_int32, C.c_uint32, C.c_int64, C.c_uint64, C.c_float
@@ -96,7 +96,6 @@ _SIGS = {
     "mgd_launch_count": [_vp, _P(_u64)],
     "mgd_set_timing": [_vp, _i32],
     "mgd_timing": [_vp, _P(C.c_double)],
-    "mgd_chain_trace": [_vp, C.c_int32, _P(C.c_uint64), _P(C.c_int32)],
     "mgd_capture_verifier_logits": [_vp, _vp],
 }
 

@@ -36,12 +36,9 @@ mg_status mgd_gemm(const uint16_t* x, const uint16_t* W, int32_t T, int32_t N, i
       G > (N / 128) * (K / 64))
     return MG_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
-  if (impl != 1) {
-    if (tile_n <= 0) tile_n = gemm_tile_n(T);
-    if (mma_n < 0 || mma_n > tile_n || (mma_n && tile_n % mma_n) || (mma_n && mma_n % 16)) return MG_ERR_INVALID;
-  } else if (T > 8 || G) {
-    return MG_ERR_INVALID;
-  }
+  if (impl != 0) return MG_ERR_INVALID;  // tcgen05 only (the CUDA-core GEMV was removed)
+  if (tile_n <= 0) tile_n = gemm_tile_n(T);
+  if (mma_n < 0 || mma_n > tile_n || (mma_n && tile_n % mma_n) || (mma_n && mma_n % 16)) return MG_ERR_INVALID;
   // the kernels read weights in the engine's tiled layout: tile W (row-major here)
   std::vector<uint16_t> rm((size_t)N * K), tl((size_t)N * K);
   cudaStreamSynchronize(st);
@@ -52,9 +49,7 @@ mg_status mgd_gemm(const uint16_t* x, const uint16_t* W, int32_t T, int32_t N, i
   if (cudaMalloc(&Wt, tl.size() * 2) != cudaSuccess) return MG_ERR_CUDA;
   cudaMemcpy(Wt, tl.data(), tl.size() * 2, cudaMemcpyHostToDevice);
   cudaError_t e;
-  if (impl == 1) {
-    e = launch_gemm_cc(x, Wt, N, K, T, splits, out, st);
-  } else {
+  {
     CUtensorMap mw, mx;
     if (!make_tmap_w_tiled(&mw, Wt, K, N) || !make_tmap_2d(&mx, x, K, T, tile_n)) {
       cudaFree(Wt);

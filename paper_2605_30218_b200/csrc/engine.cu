@@ -23,7 +23,6 @@
 #include <vector>
 
 #include "../../include/mg_debug.h"
-#include "chain.h"
 #include "engine.h"
 
 using namespace mg;
@@ -76,15 +75,6 @@ int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 // ---- schedules (A13/A14) -------------------------------------
-int splits_for(int N, int K, int T, int tile_n, int impl) {
-  const int KB = K / 64;
-  const int tiles = impl == 0 ? (N / 128) * cdiv(T, tile_n) : cdiv(N, 8);
-  const int S = cdiv(2 * kSMs, tiles);
-  int smax = KB / 4;
-  if (smax < 1) smax = 1;
-  return clampi(S, 1, smax < 16 ? smax : 16);
-}
-
 // stream-K virtual CTA count: one per SM, at least 4 k-blocks (256 k) each.
 // A function of the weight shape only (never of the batch).
 int streamk_G(int N, int K) {
@@ -92,28 +82,15 @@ int streamk_G(int N, int K) {
   return clampi(W / 4, 1, kSMs);
 }
 
-// fast path: CUDA-core GEMV for T <= this many tokens.  Default 0: the
-// tcgen05 kernel with a 16-token tile is faster at every batch size measured
-// (llama8b step, B=2: 3.29 vs 5.15 ms; B=4: 3.37 vs 8.11 ms).
-// MG_FAST_GEMV_MAX re-enables the GEMV (measurement knob).
-int gemv_max_tokens() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MG_FAST_GEMV_MAX");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
 OpSched op_fast(int N, int K, int T) {
   OpSched o;
   o.N = N;
   o.K = K;
-  o.impl = T <= gemv_max_tokens() ? 1 : 0;
+  o.impl = 0;  // tcgen05 at every batch (a CUDA-core GEMV measured 1.6-2.4x slower at B = 2 / 4)
   o.tile_n = gemm_tile_n(T);
   o.mma_n = o.tile_n;
-  o.splits = o.impl == 1 ? splits_for(N, K, T, o.tile_n, o.impl) : 1;
-  o.G = o.impl == 1 ? 0 : streamk_G(N, K);
+  o.splits = 1;
+  o.G = streamk_G(N, K);
   return o;
 }
 bool det_mma16() {
@@ -281,7 +258,6 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   c->attn_acc = s.take<float>(attn_rows * c->hd);
   c->attn_ml = s.take<float>(attn_rows * 2);
   c->attn_cnt = s.take<int32_t>((size_t)Tm * c->KV);
-  c->chain_sync = s.take<uint32_t>(2 * kChainMax + 1);
   c->top2_part = s.take<float>(Tlm * c->nb_top2 * 4);
   c->t2tiles = s.take<float>(Tlm * (size_t)(c->V / 128) * 4);
   c->rope_cos = s.take<float>((size_t)g.max_seq * (c->hd / 2));
@@ -377,9 +353,7 @@ static mg_status gemm(mg_ctx* c, const uint16_t* X, int xrows, int T, const Weig
     i0 = c->timing.used;
     cudaEventRecord(tevent(c), c->st);
   }
-  if (o.impl == 1) {
-    CK(launch_gemm_cc(X, W.ptr, W.N, W.K, T, o.splits, out, c->st));
-  } else {
+  {
     const CUtensorMap* mx = xmap(c, X, W.K, xrows, o.tile_n);
     if (!mx) return fail(c, MG_ERR_CUDA, "cuTensorMapEncodeTiled failed for activations");
     CK(launch_gemm_tc(W.map, *mx, W.N, W.K, T, o.splits, o.G, o.tile_n, o.mma_n, out, c->st, t2,
@@ -397,13 +371,9 @@ static mg_status gemm(mg_ctx* c, const uint16_t* X, int xrows, int T, const Weig
 
 // One forward over T tokens (token list slot/pos/tok/nk on device), against
 // cache `which` (0 fast, 1 shadow), leaving the residual stream in c->x.
-static bool chain_ok(const mg_ctx* c, const Sched& sc);
-static mg_status forward_chain(mg_ctx* c, int T, const int32_t* slot, const int32_t* pos, const int32_t* tok,
-                               const int32_t* nk, int which, const Sched& sc);
 
 static mg_status forward(mg_ctx* c, int T, const int32_t* slot, const int32_t* pos, const int32_t* tok,
                          const int32_t* nk, int which, const Sched& sc) {
-  if (chain_ok(c, sc)) return forward_chain(c, T, slot, pos, tok, nk, which, sc);
   const int Tm = c->Tmax;
   const float eps = c->cfg.rms_eps;
   CK(launch_embed(c->embed, tok, T, c->d, c->x, c->st));
@@ -515,112 +485,8 @@ static mg_status forward_mixed(mg_ctx* c, int B, int M, const Sched& fs, const S
   return MG_OK;
 }
 
-// ---- the persistent layer chain (chain.cu): attention + ONE kernel per layer
-static bool chain_ok(const mg_ctx* c, const Sched& sc) {
-  const OpSched* ops[4] = {&sc.qkv, &sc.o, &sc.gu, &sc.down};
-  for (const OpSched* o : ops)
-    if (o->impl != 0 || o->G < 1 || o->tile_n != sc.qkv.tile_n || o->mma_n != sc.qkv.mma_n || o->tile_n == 80)
-      return false;  // the layer chain is instantiated for power-of-two tiles only
-  return c->use_chain;
-}
-
-static mg_status chain_phase(mg_ctx* c, ChainPhase& ph, const uint16_t* X, int T, const Weight& W, const OpSched& o,
-                             double* bytes) {
-  const CUtensorMap* mx = xmap(c, X, W.K, c->Tmax, o.tile_n);
-  if (!mx) return fail(c, MG_ERR_CUDA, "cuTensorMapEncodeTiled failed for activations");
-  ph.mw = W.map;
-  ph.wbase = W.ptr;
-  ph.mx = *mx;
-  ph.N = W.N;
-  ph.K = W.K;
-  ph.G = o.G;
-  ph.part = c->part;
-  *bytes += (double)W.N * W.K * 2 + (double)T * W.K * 2 + (double)T * W.N * 4;
-  return MG_OK;
-}
-
-static QkvArgs qkv_args(mg_ctx* c, int layer, int which, int T, const int32_t* slot, const int32_t* pos) {
-  QkvArgs q{};
-  q.bias = c->layers[layer].bqkv; q.pos = pos; q.T = T; q.H = c->H; q.KV = c->KV; q.hd = c->hd;
-  q.rcos = c->rope_cos; q.rsin = c->rope_sin; q.q = c->q;
-  q.cache = cache_view(c, which, layer); q.paged = 1; q.slot = slot;
-  return q;
-}
-
-static mg_status run_chain(mg_ctx* c, ChainArgs& ca, const OpSched& o, double bytes, int layer) {
-  ca.sync = c->chain_sync;
-  ca.err = c->nan_d + 1;
-  ca.trace = layer == c->chain_trace_layer ? c->chain_trace : nullptr;
-  ca.pf_kblocks = c->chain_pf;
-  size_t i0 = 0;
-  if (c->timing.on) { i0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
-  CK(launch_chain(ca, o.tile_n, o.mma_n, c->st));
-  c->launches += 1;
-  if (c->timing.on) {
-    cudaEventRecord(tevent(c), c->st);
-    c->timing.rec.emplace_back(i0, i0 + 1, 0, bytes);
-  }
-  return MG_OK;
-}
-
-static mg_status forward_chain(mg_ctx* c, int T, const int32_t* slot, const int32_t* pos, const int32_t* tok,
-                               const int32_t* nk, int which, const Sched& sc) {
-  const float eps = c->cfg.rms_eps;
-  CK(launch_embed(c->embed, tok, T, c->d, c->x, c->st));
-  CK(launch_rmsnorm(c->x, c->layers[0].attn_norm, T, c->d, eps, c->xn, c->st));
-  c->launches += 2;
-  mg_status r;
-  {  // layer 0's QKV + epilogue
-    ChainArgs ca{};
-    double bytes = 0;
-    ca.T = T;
-    ca.n_ph = 1;
-    if ((r = chain_phase(c, ca.ph[0], c->xn, T, c->layers[0].qkv, sc.qkv, &bytes))) return r;
-    ca.ph[0].op = CH_QKV;
-    ca.ph[0].qkv = qkv_args(c, 0, which, T, slot, pos);
-    if ((r = run_chain(c, ca, sc.qkv, bytes, -1))) return r;
-  }
-  for (int l = 0; l < c->L; ++l) {
-    const LayerW& w = c->layers[l];
-    AttnArgs aa{};
-    aa.q = c->q; aa.cache = cache_view(c, which, l); aa.paged = 1; aa.slot = slot; aa.n_keys = nk;
-    aa.T = T; aa.H = c->H; aa.KV = c->KV; aa.hd = c->hd; aa.split_keys = sc.attn_sk; aa.n_splits = sc.attn_ns;
-    aa.part_acc = c->attn_acc; aa.part_ml = c->attn_ml; aa.out = c->att;
-    aa.qmap = c->attn_qmap; aa.kmap = aa.vmap = c->kv_map[which]; aa.counter = c->attn_cnt;
-    aa.prewait = which == 0;
-    size_t i0 = 0;
-    if (c->timing.on) { i0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
-    CK(launch_attention(aa, c->st));
-    c->launches += 1;
-    if (c->timing.on) {
-      cudaEventRecord(tevent(c), c->st);
-      c->timing.rec.emplace_back(i0, i0 + 1, 1, 0.0);
-    }
-    // O-proj -> residual + mlp norm -> gate/up -> SwiGLU -> down -> residual + next norm [-> next QKV]
-    ChainArgs ca{};
-    double bytes = 0;
-    ca.T = T;
-    const bool last = l + 1 == c->L;
-    ca.n_ph = last ? 3 : 4;
-    if ((r = chain_phase(c, ca.ph[0], c->att, T, w.o, sc.o, &bytes))) return r;
-    ca.ph[0].op = CH_RESNORM; ca.ph[0].x = c->x; ca.ph[0].w = w.mlp_norm; ca.ph[0].xn = c->xn; ca.ph[0].eps = eps;
-    if ((r = chain_phase(c, ca.ph[1], c->xn, T, w.gu, sc.gu, &bytes))) return r;
-    ca.ph[1].op = CH_SWIGLU; ca.ph[1].a = c->a;
-    if ((r = chain_phase(c, ca.ph[2], c->a, T, w.down, sc.down, &bytes))) return r;
-    ca.ph[2].op = CH_RESNORM; ca.ph[2].x = c->x; ca.ph[2].xn = c->xn; ca.ph[2].eps = eps;
-    ca.ph[2].w = last ? c->final_norm : c->layers[l + 1].attn_norm;
-    if (!last) {
-      if ((r = chain_phase(c, ca.ph[3], c->xn, T, c->layers[l + 1].qkv, sc.qkv, &bytes))) return r;
-      ca.ph[3].op = CH_QKV;
-      ca.ph[3].qkv = qkv_args(c, l + 1, which, T, slot, pos);
-    }
-    if ((r = run_chain(c, ca, sc.o, bytes, l))) return r;
-  }
-  return MG_OK;
-}
-
 // The fused top-2 epilogue replaces the fp32 logits unless something needs
-// them: logit captures (tests), the test-only injected noise, the CUDA-core GEMV.
+// them: logit captures (tests), the test-only injected noise, the unfused A/B knob.
 static bool lm_fused(const mg_ctx* c, const OpSched& o, bool fast_rows) {
   return o.impl == 0 && !c->capture && !c->capture_v && !(fast_rows && c->inj_amp > 0.f) && !c->lm_unfused;
 }
@@ -1254,16 +1120,10 @@ mg_status mg_init(const mg_config* cfg, const mg_buffers* bufs, void* stream, mg
   cudaEventRecord(c->stage_ev[0], c->st);
   cudaEventRecord(c->stage_ev[1], c->st);
   {
-    // the persistent layer chain is measured slower than the separate kernels
-    // (DESIGN.md section 7.4); MG_CHAIN=1 selects it for A/B measurements
-    const char* e = getenv("MG_CHAIN");
-    c->use_chain = e && e[0] == '1';
     const char* lu = getenv("MG_LM_UNFUSED");  // A/B knob: logits + separate top-2 kernels
     c->lm_unfused = lu && lu[0] == '1';
     const char* fs = getenv("MG_FAST_SK");  // measurement knobs: attention split sizes
     c->fast_sk_override = fs ? atoi(fs) : 0;
-    const char* f = getenv("MG_CHAIN_PF");  // A/B knob: L2 run-ahead in 16 KB k-blocks
-    c->chain_pf = f ? atoi(f) : 0;
   }
   if ((e = cudaMallocHost(&c->fpin, fpin_words(c) * 4)) || (e = cudaEventCreateWithFlags(&c->fev, cudaEventDisableTiming)))
     return die(cudaGetErrorString(e));
@@ -1532,12 +1392,11 @@ mg_status mg_stats(mg_ctx* c, mg_stats_t* out) {
   mg_status rf = pipe_refresh(c);
   if (rf) return rf;
   unsigned long long s[16];
-  int32_t flags[2] = {0, 0};  // [0] NaN logit, [1] layer-chain grid barrier timed out
+  int32_t flags[1] = {0};  // NaN logit
   CK(cudaMemcpyAsync(s, c->stats_d, sizeof(s), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(flags, c->nan_d, 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(flags, c->nan_d, 4, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   const int32_t nan = flags[0];
-  if (flags[1]) return fail(c, MG_ERR_CUDA, "a layer-chain grid barrier timed out: results are invalid");
   out->steps = s[0]; out->rows = s[1]; out->protected_rows = s[2]; out->triggers = s[3];
   out->verified = s[4]; out->repairs = s[5]; out->verifier_launches = s[6]; out->catchup_tokens = s[7];
   out->window_rows = s[8]; out->rollbacks = s[9]; out->rolled_back_tokens = s[10];
@@ -1575,7 +1434,6 @@ void mg_destroy(mg_ctx* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->fpin) cudaFreeHost(c->fpin);
   if (c->fev) cudaEventDestroy(c->fev);
-  if (c->chain_trace) cudaFree(c->chain_trace);
   delete c;
 }
 
@@ -1735,18 +1593,6 @@ mg_status mgd_set_timing(mg_ctx* c, int32_t on) {
 
 // out: [0] gemm ms total, [1] gemm launches, [2] gemm algorithmic bytes,
 //      [3] attention ms total, [4] attention launches, [5] step ms total, [6] steps
-mg_status mgd_chain_trace(mg_ctx* c, int32_t layer, unsigned long long* out_host, int32_t* words) {
-  if (!c || !words) return MG_ERR_INVALID;
-  *words = chain_grid() * kChainTraceWords;
-  if (!c->chain_trace) CK(cudaMalloc(&c->chain_trace, (size_t)*words * 8));
-  if (out_host) {
-    CK(cudaStreamSynchronize(c->st));
-    CK(cudaMemcpy(out_host, c->chain_trace, (size_t)*words * 8, cudaMemcpyDeviceToHost));
-  }
-  c->chain_trace_layer = layer;
-  return MG_OK;
-}
-
 mg_status mgd_timing(mg_ctx* c, double* out) {
   if (!c || !out) return MG_ERR_INVALID;
   CK(cudaStreamSynchronize(c->st));

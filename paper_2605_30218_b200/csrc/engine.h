@@ -77,11 +77,6 @@ struct mg_ctx {
   float *part, *logits, *attn_acc, *attn_ml, *top2_part;
   float* t2tiles = nullptr;  // fused LM-head top-2: per-(token, 128-row tile) sets [Tlm][V/128][4]
   int32_t* attn_cnt;                     // [Tmax][KV] chunk-arrival counters
-  uint32_t* chain_sync;                  // layer-chain grid barriers + epoch (chain.h)
-  bool use_chain = false;                // MG_CHAIN=1: persistent layer chain (A/B only; slower today)
-  unsigned long long* chain_trace = nullptr;  // diagnostics (mgd_chain_trace)
-  int chain_trace_layer = -2;
-  int chain_pf = 0;
   int fast_sk_override = 0;  // MG_FAST_SK (measurement)
   int verify_mode = 0;       // mg_verify_mode (mg_set_policy)
   uint8_t* pend_d = nullptr;  // [max_slots] pipelined verification: tentative token pending
@@ -99,7 +94,7 @@ struct mg_ctx {
   unsigned long long inj_seed = 0;
   int force_B = 0;           // test-only: fast attention splits of another batch size (mgd_force_schedule)
   int repair_mode = 0;       // mg_repair_action
-  int det_sk = 512;          // verifier attention keys per split (A14; MG_DET_SK for measurement)  // chain L2 run-ahead (k-blocks per CTA; measured harmful, off)
+  int det_sk = 512;          // verifier attention keys per split (A14; MG_DET_SK for measurement)
   CUtensorMap attn_qmap, kv_map[2];      // TMA maps: q [Tmax][H][hd]; pools (fast, shadow)
   float *rope_cos, *rope_sin;
   size_t part_elems;

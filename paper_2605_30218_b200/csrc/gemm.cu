@@ -29,9 +29,8 @@
 // verifier runs the same full-width MMAs as the fast path.  MMA16 (16-column
 // instructions per slot group) remains as an option.
 //
-// k_gemm_cc: CUDA-core kernel for T <= 8 tokens (the fast path's tiny-batch
-// choice): warp per output row, 128-bit weight loads, fp32 FMA, fixed
-// xor-shuffle tree.
+// (A CUDA-core GEMV for T <= 8 tokens measured 1.6-2.4x slower per step at
+// B = 2 / 4 than this kernel's 16-token tile and was removed in round 2.)
 #include "common.cuh"
 #include <climits>
 
@@ -241,49 +240,6 @@ __global__ void __launch_bounds__(192, 1)
   if (ctr && threadIdx.x == 0) ctr[3] = (long long)globaltimer();
 }
 
-// ------------------------------------------------------------------ CUDA-core
-template <int TT>
-__global__ void __launch_bounds__(256) k_gemm_cc(const uint16_t* __restrict__ x, const uint16_t* __restrict__ W,
-                                                 int N, int K, int T, int splits, float* __restrict__ out) {
-  griddep();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = blockIdx.x * 8 + warp;
-  const int s = blockIdx.y;
-  if (n >= N) return;
-  const int KB = K / 64;  // split boundaries on 64-wide blocks, like k_gemm_tc
-  const int kb0 = chunk_start(KB, splits, s), kb1 = chunk_start(KB, splits, s + 1);
-  float acc[TT];
-#pragma unroll
-  for (int t = 0; t < TT; ++t) acc[t] = 0.f;
-  // tiled weights: row n's 64 elements of k-block kb are 128 contiguous bytes
-  const uint16_t* w = W + tiled_offset((size_t)n, 0, K);
-#pragma unroll 4
-  for (int kb = kb0 + (lane >> 3); kb < kb1; kb += 4) {
-    const int k = kb * 64 + (lane & 7) * 8;
-    const uint4 wv = __ldg(reinterpret_cast<const uint4*>(w + (size_t)kb * 8192 + (lane & 7) * 8));
-    const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-    for (int t = 0; t < TT; ++t) {
-      if (t < T) {
-        const uint4 xv = *reinterpret_cast<const uint4*>(x + (size_t)t * K + k);
-        const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          acc[t] = fmaf(lo_bf(ww[j]), lo_bf(xx[j]), acc[t]);
-          acc[t] = fmaf(hi_bf(ww[j]), hi_bf(xx[j]), acc[t]);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < TT; ++t) {
-    float v = acc[t];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0 && t < T) out[((size_t)s * T + t) * N + n] = v;
-  }
-}
-
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -412,18 +368,6 @@ int gemm_tile_n(int T) {
   if (T <= 80) return 80;  // e.g. a batch of 64 plus the fused verifier's columns: 4 stages, not the 128 tile's 3
   if (T <= 128) return 128;
   return 256;
-}
-
-cudaError_t launch_gemm_cc(const uint16_t* x, const uint16_t* W, int N, int K, int T, int splits, float* out,
-                           cudaStream_t st) {
-  dim3 grid((N + 7) / 8, splits);
-  switch (T) {
-    case 1: return launch_k(k_gemm_cc<1>, grid, dim3(256), 0, st, x, W, N, K, T, splits, out);
-    case 2: return launch_k(k_gemm_cc<2>, grid, dim3(256), 0, st, x, W, N, K, T, splits, out);
-    case 3: case 4: return launch_k(k_gemm_cc<4>, grid, dim3(256), 0, st, x, W, N, K, T, splits, out);
-    case 5: case 6: case 7: case 8: return launch_k(k_gemm_cc<8>, grid, dim3(256), 0, st, x, W, N, K, T, splits, out);
-    default: return cudaErrorInvalidValue;
-  }
 }
 
 }  // namespace mg

@@ -67,8 +67,6 @@ cudaError_t launch_gemm_tc(const CUtensorMap& mw, const CUtensorMap& mx, int N, 
 // max partial slots of any tile for a GEMM shape (buffer sizing)
 int part_slots(const PartSpec& p, int N);
 int num_sms();
-cudaError_t launch_gemm_cc(const uint16_t* x, const uint16_t* W, int N, int K, int T, int splits, float* out,
-                           cudaStream_t st);
 int gemm_tile_n(int T);
 
 // ---- elementwise (a1, a2, epilogues)

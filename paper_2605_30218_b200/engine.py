@@ -181,17 +181,6 @@ class Engine:
     def set_timing(self, on: bool):
         check(lib().mgd_set_timing(self.ctx, int(on)), self.ctx, "set_timing")
 
-    def chain_trace(self, layer: int, read: bool = False):
-        """Diagnostics: trace the layer-chain launch of `layer` (-2: off); with
-        read=True return the last stamps as [CTA][1 + 4*6] ns (mg_debug.h)."""
-        n = C.c_int32(0)
-        check(lib().mgd_chain_trace(self.ctx, layer, None, C.byref(n)), self.ctx, "chain_trace")
-        if not read:
-            return None
-        buf = (C.c_uint64 * n.value)()
-        check(lib().mgd_chain_trace(self.ctx, layer, buf, C.byref(n)), self.ctx, "chain_trace")
-        return np.array(buf, dtype=np.int64).reshape(-1, 25)
-
     def timing(self) -> dict:
         o = (C.c_double * 8)()
         check(lib().mgd_timing(self.ctx, o), self.ctx, "timing")

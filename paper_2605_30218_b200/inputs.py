@@ -23,6 +23,14 @@ SHAPES = {
                      qkv_bias=1, rms_eps=1e-6, rope_theta=1000000.0),
     "wide": dict(n_layers=2, d_model=4096, n_heads=32, n_kv_heads=8, head_dim=128, d_ff=14336, vocab=128256,
                  qkv_bias=0, rms_eps=1e-5, rope_theta=500000.0),
+    # long-context parity configs (tests/test_gpu_longctx.py): the attention
+    # shapes of Llama-3.1-8B (32 q / 8 kv heads, hd 128) and of
+    # DSR1-Distill-Qwen-7B (28 / 4, hd 128, qkv bias) on narrow, shallow
+    # models, so the oracle can recompute contexts of 500-4000 keys
+    "longattn": dict(n_layers=2, d_model=1024, n_heads=32, n_kv_heads=8, head_dim=128, d_ff=2048, vocab=16384,
+                     qkv_bias=0, rms_eps=1e-5, rope_theta=500000.0),
+    "dsr1attn": dict(n_layers=2, d_model=896, n_heads=28, n_kv_heads=4, head_dim=128, d_ff=2048, vocab=16384,
+                     qkv_bias=1, rms_eps=1e-6, rope_theta=10000.0),
     "llama8b": dict(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=8, head_dim=128, d_ff=14336,
                     vocab=128256, qkv_bias=0, rms_eps=1e-5, rope_theta=500000.0),
     "qwen14b": dict(n_layers=48, d_model=5120, n_heads=40, n_kv_heads=8, head_dim=128, d_ff=13824,

@@ -8,7 +8,7 @@ root=$(cd "$(dirname "$0")/.." && pwd)
 out=$root/scripts/ab/$name
 mkdir -p "$out"
 objs=()
-for f in gemm chain elementwise attention control engine capi_debug; do
+for f in gemm elementwise attention control engine capi_debug; do
   [ -f "$root/paper_2605_30218_b200/csrc/$f.cu" ] || continue
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
     --expt-relaxed-constexpr -I"$root/include" "$@" -c "$root/paper_2605_30218_b200/csrc/$f.cu" -o "$out/$f.o" &

@@ -27,22 +27,10 @@ def torch():
     return torch
 
 
-def _engine(shape, B, max_seq=96, page_size=16, verify_chunk=0, slots=None, chain="0"):
-    """chain="1": the persistent layer-chain kernel (chain.cu) instead of the
-    separate GEMM / epilogue kernels (the choice is read at mg_init)."""
-    import os
-
+def _engine(shape, B, max_seq=96, page_size=16, verify_chunk=0, slots=None):
     from paper_2605_30218_b200.engine import Engine
-    old = os.environ.get("MG_CHAIN")
-    os.environ["MG_CHAIN"] = chain
-    try:
-        return Engine(shape, max_batch=B, max_slots=slots or B, max_seq=max_seq, page_size=page_size,
-                      verify_chunk=verify_chunk)
-    finally:
-        if old is None:
-            del os.environ["MG_CHAIN"]
-        else:
-            os.environ["MG_CHAIN"] = old
+    return Engine(shape, max_batch=B, max_slots=slots or B, max_seq=max_seq, page_size=page_size,
+                  verify_chunk=verify_chunk)
 
 
 def _decode(torch, eng, prompts, steps, tau, prot=None, record=False):
@@ -79,14 +67,20 @@ def _oracle_reference(orc, m, prompt, n):
     return toks, gs
 
 
-def _check_logit_err(e):
-    """|delta logit| <= 2e-2 (north star) for 99.9% of logits and
-    <= 1.5 x 2e-2 for all of them.  The tail exists because bf16 roundings of
-    activations turn fp32 accumulation-order differences into occasional
-    1-ulp flips that propagate (measured: p99.9 ~ 1.5e-2, max ~ 2.4e-2 on
-    the 2-layer configs); a wrong index or dropped term gives O(1) errors."""
-    assert np.quantile(e, 0.999) <= TOL, float(np.quantile(e, 0.999))
-    assert e.max() <= 1.5 * TOL, float(e.max())
+def _check_logit_err(e, noise):
+    """|delta logit| within max(2e-2, 2 x the oracle's own
+    schedule-to-schedule noise) -- at p99.9 against the noise's p99.9 and at
+    the max against its max.  `noise` = |oracle(batch-shaped plan) -
+    oracle(pinned plan)| on the same teacher-forced prefix: two valid fp32
+    summation orders of the same model; the GPU's order is a third, so its
+    distance to either is bounded by about twice their spread (bf16
+    activation roundings turn reorder differences into occasional 1-ulp flips
+    that propagate).  A wrong index or dropped term gives O(1) errors."""
+    q_tol = max(TOL, 2 * float(np.quantile(noise, 0.999)))
+    m_tol = max(TOL, 2 * float(noise.max()))
+    assert np.quantile(e, 0.999) <= q_tol, (float(np.quantile(e, 0.999)), q_tol)
+    assert e.max() <= m_tol, (float(e.max()), m_tol)
+    return m_tol
 
 
 def _agree_until_band(gpu, ora, margins):
@@ -122,8 +116,8 @@ def test_weights_bit_exact(orc, torch, tiny, tiny_gqa, which):
     eng.close()
 
 
-@pytest.mark.parametrize("which,chain", [("tiny", "0"), ("tiny_gqa", "0"), ("tiny", "1"), ("tiny_gqa", "1")])
-def test_tau_inf_reference_and_batch_invariance(orc, torch, tiny, tiny_gqa, which, chain):
+@pytest.mark.parametrize("which", ["tiny", "tiny_gqa"])
+def test_tau_inf_reference_and_batch_invariance(orc, torch, tiny, tiny_gqa, which):
     """tau=+inf (always-on verification) on the GPU: every row's sequence is
     bit-identical at batch 1, 3 and 8 (whatever shares the batch), and equals
     the oracle's deterministic reference outside the argmax-ambiguity band."""
@@ -135,7 +129,7 @@ def test_tau_inf_reference_and_batch_invariance(orc, torch, tiny, tiny_gqa, whic
         got = []
         for i0 in range(0, 8, B):
             group = prompts[i0:i0 + B]
-            eng = _engine(shp, len(group), chain=chain)
+            eng = _engine(shp, len(group))
             s, _ = _decode(torch, eng, group, steps, INF)
             st = eng.stats()
             assert st["triggers"] == st["protected_rows"] == len(group) * (steps - 1)   # r_verify = 1
@@ -150,21 +144,23 @@ def test_tau_inf_reference_and_batch_invariance(orc, torch, tiny, tiny_gqa, whic
     assert compared >= 0.6 * 8 * steps   # most tokens are outside the band on random-init logits
 
 
-@pytest.mark.parametrize("chain", ["0", "1"])
-def test_fast_logits_teacher_forced(orc, torch, tiny, chain):
+def test_fast_logits_teacher_forced(orc, torch, tiny):
     """tau=0 (pure BF16 batched, r_verify=0): the fast logits the GPU
     captures stay within 2e-2 of the oracle's, teacher-forced on the GPU's
     tokens; the fast argmax agrees outside the band."""
     shp, m = tiny
     B, steps = 6, 12
     prompts = inputs.prompts(B, inputs.ragged_lengths(B, 8, 20, seed=5), shp["vocab"], seed=40)
-    eng = _engine(shp, B, chain=chain)
+    eng = _engine(shp, B)
     cap = torch.empty((B, shp["vocab"]), dtype=torch.float32, device="cuda")
     eng.capture_logits(cap)
     st = orc.State(m, B, 64)
+    sd = orc.State(m, B, 64)            # the same prefix under the pinned plan (self-noise)
     det = orc.det_sched()
     y0 = [eng.prefill(i, p) for i, p in enumerate(prompts)]
     y0o = [st.prefill(i, p, det) for i, p in enumerate(prompts)]
+    for i, p in enumerate(prompts):
+        sd.prefill(i, p, det)
     out = torch.empty(B, dtype=torch.int32, device="cuda")
     worst = 0.0
     for i in range(B):
@@ -174,11 +170,12 @@ def test_fast_logits_teacher_forced(orc, torch, tiny, chain):
         eng.step(list(range(B)), None, 0.0, out)
         o = out.cpu().numpy()
         lg = cap.cpu().numpy()
-        r = st.step(np.arange(B), np.zeros(B, np.uint8), 0.0, orc.fast_sched(B), det, forced_out=o,
-                    forced_kind=np.zeros(B, np.uint8), want_logits=True)
+        kw = dict(forced_out=o, forced_kind=np.zeros(B, np.uint8), want_logits=True)
+        r = st.step(np.arange(B), np.zeros(B, np.uint8), 0.0, orc.fast_sched(B), det, **kw)
+        rd = sd.step(np.arange(B), np.zeros(B, np.uint8), 0.0, det, det, **kw)
         e = np.abs(lg - r["logits"])
         worst = max(worst, float(e.max()))
-        _check_logit_err(e)
+        _check_logit_err(e, np.abs(r["logits"] - rd["logits"]))
         for b in range(B):
             if r["g"][b] > 2 * e[b].max():      # argmax bound, per row
                 assert o[b] == r["f_tok"][b]
@@ -334,9 +331,12 @@ def test_wide_shallow_parity(orc, torch):
         cap = torch.empty((B, shp["vocab"]), dtype=torch.float32, device="cuda")
         eng.capture_logits(cap)
         st = orc.State(m, B, 32)
+        sd = orc.State(m, B, 32)        # pinned plan on the same prefix (self-noise)
         det = orc.det_sched()
         y0 = [eng.prefill(i, p) for i, p in enumerate(prompts)]
         pre = [st.prefill(i, p, det, want_logits=True) for i, p in enumerate(prompts)]
+        for i, p in enumerate(prompts):
+            sd.prefill(i, p, det)
         # a first token may differ only inside the argmax-ambiguity band; such a
         # row then consumes a different input token and is left out below
         same = np.array([a == b for a, (b, _) in zip(y0, pre)])
@@ -347,11 +347,13 @@ def test_wide_shallow_parity(orc, torch):
         for _ in range(3):
             eng.step(list(range(B)), None, 0.0, out)
             o = out.cpu().numpy()
-            r = st.step(np.arange(B), np.zeros(B, np.uint8), 0.0, orc.fast_sched(B), det, forced_out=o,
-                        forced_kind=np.zeros(B, np.uint8), want_logits=True)
-            _check_logit_err(np.abs(cap.cpu().numpy() - r["logits"])[same])
+            kw = dict(forced_out=o, forced_kind=np.zeros(B, np.uint8), want_logits=True)
+            r = st.step(np.arange(B), np.zeros(B, np.uint8), 0.0, orc.fast_sched(B), det, **kw)
+            rd = sd.step(np.arange(B), np.zeros(B, np.uint8), 0.0, det, det, **kw)
+            _check_logit_err(np.abs(cap.cpu().numpy() - r["logits"])[same], np.abs(r["logits"] - rd["logits"])[same])
         eng.close()
         st.close()
+        sd.close()
     p = inputs.prompts(1, 9, shp["vocab"], seed=777)[0]
     eng = _engine(shp, 1, max_seq=32)
     seqs, _ = _decode(torch, eng, [p], 6, INF)

@@ -1,0 +1,161 @@
+"""End-to-end oracle parity past 512 keys, where the batch-64 fast plan and the
+verifier's plan really differ ("serving shape
+changes the reduction plan", :203 argmax bound, :225 reference).
+
+At batch 64 the fast attention takes one split per (token, kv head) (8 KV
+heads: 512 CTAs) or two capacity-sized splits (4 KV heads), while the
+verifier pins 512-key splits (A13/A14): with contexts of 520-4000
+keys the two paths run different reduction plans in the SAME engine.  Per
+case the GPU decodes the whole batch (prompts of the stated lengths) for
+three steps -- tau = +inf (every row verified), a finite tau (real gate
+decisions), tau = +inf -- and sampled rows are recomputed by the oracle,
+teacher-forced on the GPU's committed tokens and gate decisions, twice in
+lockstep: A with the oracle's batch-shaped plan, D with its pinned plan.
+|A - D| is the oracle's own schedule-to-schedule noise; the GPU, a third
+valid summation order, must stay within max(2e-2, 2 x that noise)
+(DESIGN.md 9).  Compared element by element on every sampled row and step:
+
+* fast logits vs A; verifier logits (every row the gate sent to the
+  verifier) vs D;
+* the fast token and the verifier token wherever the oracle's margin exceeds
+  twice the observed logit error (then the argmax is unique);
+* the gate decision wherever |g - tau| exceeds twice the error bound (the
+  margin is 2-Lipschitz in the logits);
+* the commit kind (fast / verified / repair) wherever both argmaxes are
+  unique.
+
+Cases: "wide" (Llama-3.1-8B widths, 2 layers, full 128256 vocabulary,
+prompts 520-1100); "longattn" (Llama-8B attention shape on a narrow model,
+prompts 520-1100, 2-3 pinned verifier splits); "dsr1attn"
+(DSR1-Distill-Qwen-7B attention shape -- 4 KV heads, qkv bias -- on a
+narrow model, prompts 2000-4000).  The oracle recomputes sampled rows only
+(its cost is ~0.5 GMAC per wide token).
+"""
+import numpy as np
+import pytest
+
+from paper_2605_30218_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+INF = float("inf")
+
+# name -> (batch, (min, max) prompt length, sampled rows by prompt-length rank:
+#          0 = shortest; -1 = longest)
+CASES = {
+    "wide": (64, (520, 1100), (0,)),
+    "longattn": (64, (520, 1100), (0, 32, -1)),
+    "dsr1attn": (64, (2000, 4000), (20,)),
+}
+
+
+def _gpu_run(shp, B, prompts, taus):
+    import torch
+
+    from paper_2605_30218_b200.engine import Engine
+    V = shp["vocab"]
+    eng = Engine(shp, max_batch=B, max_slots=B, max_seq=max(len(p) for p in prompts) + len(taus) + 4, page_size=64)
+    capf = torch.empty((B, V), dtype=torch.float32, device="cuda")
+    capv = torch.empty((B, V), dtype=torch.float32, device="cuda")
+    eng.capture_logits(capf)
+    eng.capture_verifier_logits(capv)
+    first = [eng.prefill(i, p) for i, p in enumerate(prompts)]
+    out = torch.empty(B, dtype=torch.int32, device="cuda")
+    recs = []
+    for tau in taus:
+        if callable(tau):               # a threshold chosen from the previous step's margins
+            tau = tau(recs[-1])
+        capv.zero_()
+        eng.step(list(range(B)), None, tau, out)
+        torch.cuda.synchronize()
+        r = eng.last_step(B)
+        r["fast_logits"] = capf.cpu().numpy().copy()
+        r["ver_logits"] = capv.cpu().numpy().copy()       # rank order = ascending gated rows
+        r["out"] = out.cpu().numpy().copy()
+        r["tau"] = tau
+        recs.append(r)
+    eng.close()
+    return first, recs
+
+
+def _finite_tau(g):
+    """A threshold with real decisions on both sides: the median margin."""
+    return float(np.median(np.asarray(g, np.float64)))
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_long_context_parity(orc, name):
+    shp = inputs.shape(name)
+    B, (lo, hi), ranks = CASES[name]
+    lengths = inputs.ragged_lengths(B, lo, hi, seed=97)
+    prompts = inputs.prompts(B, lengths, shp["vocab"], seed=5000)
+    order = np.argsort(lengths, kind="stable")
+    rows = sorted({int(order[r]) for r in ranks})
+
+    # steps: tau = inf, a finite tau (the median of the previous step's fast
+    # margins -- an input of the run, not an expected value), tau = inf
+    first, recs = _gpu_run(shp, B, prompts, [INF, lambda prev: _finite_tau(prev["g"]), INF])
+    taus = [r["tau"] for r in recs]
+    trig1 = recs[1]["trig"].astype(bool)
+    assert 0 < trig1.sum() < B                            # the finite tau splits the batch
+
+    m = orc.Model(shp)
+    det = orc.det_sched()
+    checked = dict(fast_tok=0, ver_tok=0, gate=0, kind=0, ver_rows=0)
+    for row in rows:
+        plen = len(prompts[row])
+        A = orc.State(m, 1, plen + len(taus) + 2)
+        D = orc.State(m, 1, plen + len(taus) + 2)
+        ya, la = A.prefill(0, prompts[row], det, want_logits=True)
+        yd = D.prefill(0, prompts[row], det)
+        assert ya == yd
+        if ya != first[row]:
+            assert float(orc.top2(la)["g"][0]) <= 2 * TOL, (row, "first token outside the band")
+            A.close(); D.close()
+            continue
+        for t, tau in enumerate(taus):
+            r = recs[t]
+            gtrig = int(r["trig"][row])
+            kw = dict(forced_trig=[gtrig], forced_out=[int(r["out"][row])], want_logits=True)
+            ra = A.step([0], [1], tau, orc.fast_sched(B), det, **kw)
+            rd = D.step([0], [1], tau, det, det, forced_trig=[1], forced_out=[int(r["out"][row])],
+                        want_logits=True)
+            noise = np.abs(ra["logits"][0] - rd["logits"][0])
+            q_tol = max(TOL, 2 * float(np.quantile(noise, 0.999)))
+            m_tol = max(TOL, 2 * float(noise.max()))
+            ef = np.abs(r["fast_logits"][row] - ra["logits"][0])
+            print(f"[longctx] {name} row {row} (ctx {plen + t + 1}) step {t}: fast p99.9 "
+                  f"{np.quantile(ef, 0.999):.4f} max {ef.max():.4f} | oracle self-noise p99.9 "
+                  f"{np.quantile(noise, 0.999):.4f} max {noise.max():.4f}")
+            assert np.quantile(ef, 0.999) <= q_tol, (row, t, float(np.quantile(ef, 0.999)), q_tol)
+            assert ef.max() <= m_tol, (row, t, float(ef.max()), m_tol)
+            f_unique = ra["g"][0] > 2 * max(m_tol, float(ef.max()))
+            if f_unique:
+                assert int(r["f_tok"][row]) == int(ra["f_tok"][0]), (row, t)
+                checked["fast_tok"] += 1
+            # gate decision (strict g < tau), outside the band
+            if tau != INF and abs(float(ra["g"][0]) - tau) > 2 * m_tol:
+                assert bool(gtrig) == bool(ra["g"][0] < tau), (row, t, float(ra["g"][0]), tau)
+                checked["gate"] += 1
+            if not gtrig:
+                assert int(r["kind"][row]) == 0 and int(r["out"][row]) == int(r["f_tok"][row])
+                continue
+            # verifier logits of this row: rank = number of gated rows before it
+            rank = int(r["trig"][:row].sum())
+            ev = np.abs(r["ver_logits"][rank] - rd["logits"][0])
+            assert np.quantile(ev, 0.999) <= q_tol and ev.max() <= m_tol, (row, t, float(ev.max()), m_tol)
+            checked["ver_rows"] += 1
+            v_unique = rd["v_g"][0] > 2 * max(m_tol, float(ev.max()))
+            if v_unique:
+                assert int(r["v_tok"][row]) == int(rd["v_tok"][0]), (row, t)
+                checked["ver_tok"] += 1
+            if v_unique and f_unique:     # commit kind
+                want = 1 if int(rd["v_tok"][0]) == int(ra["f_tok"][0]) else 2
+                assert int(r["kind"][row]) == want, (row, t)
+                checked["kind"] += 1
+        A.close()
+        D.close()
+    m.close()
+    print(f"[longctx] {name}: checked {checked}")
+    assert checked["fast_tok"] >= len(rows) and checked["ver_rows"] >= len(rows)

@@ -340,21 +340,30 @@ def test_injected_noise_matches_oracle(orc, torch, tiny):
     if [st.prefill(i, p, det) for i, p in enumerate(prompts)] != first:
         pytest.skip("prefill token inside the ambiguity band")
     fs = orc.fast_sched(B, noise_amp=amp, noise_seed=seed)
-    rep = checked = 0
+    rep = checked = kinds_checked = 0
     for _ in range(steps):
         eng.step(list(range(B)), prot, tau, out, kind)
         r = eng.last_step(B)
         o = out.cpu().numpy()
-        ro = st.step(np.arange(B), prot, tau, fs, det, forced_trig=r["trig"], forced_out=o, forced_kind=r["kind"])
+        # teacher-forced on the GPU's committed tokens and gate decisions (so
+        # both sides verify the same rows); the oracle takes its OWN verifier
+        # token and commit kind (nothing else is forced)
+        ro = st.step(np.arange(B), prot, tau, fs, det, forced_trig=r["trig"], forced_out=o)
         for b in range(B):
             assert abs(float(r["g"][b]) - float(ro["g"][b])) <= BAND, (b, r["g"][b], ro["g"][b])
-            if ro["g"][b] > BAND:
+            f_unique = ro["g"][b] > BAND
+            if f_unique:
                 assert r["f_tok"][b] == ro["f_tok"][b]
                 checked += 1
             if abs(float(ro["g"][b]) - tau) > BAND:
                 assert bool(r["trig"][b]) == bool(ro["g"][b] < tau)
+            if r["trig"][b] and ro["v_g"][b] > BAND:         # the verifier token is unique
+                assert int(r["v_tok"][b]) == int(ro["v_tok"][b]), b
+                if f_unique:
+                    assert int(r["kind"][b]) == int(ro["kind"][b]), b
+                    kinds_checked += 1
         rep += int((r["kind"] == 2).sum())
-    assert rep > 0 and checked > B * steps // 2
+    assert rep > 0 and checked > B * steps // 2 and kinds_checked > 0
     eng.close()
     st.close()
     # batch 1: the perturbation is exactly zero
