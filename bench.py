@@ -1,10 +1,13 @@
 """bench.py -- MarginGate decode throughput on B200 (BASELINE.json configs[1]).
 
 Workload (N=1): Llama-3.1-8B-shaped random-init decoder (DESIGN.md 3.1
-weights, seed 42), batch 64 per GPU, every row protected, MATH500-shaped
-request (prompt 128 / decode 512): the timed steps run at the
-mid-decode context (ctx ~ 128 + 256).  One bench "step" = one mg_decode_step
-= one pass of the whole hot path over the batch.
+weights, seed 42), batch 64 per GPU, MATH500-shaped request (prompt 128 /
+decode 512): the K timed steps are the LAST K steps of that
+decode (contexts up to 640), past the verifier's 512-key attention split, where
+the batch-64 fast plan and the verifier's pinned plan differ
+and MarginGate's gate has real work (calibrated tau100 > 0).  One bench
+"step" = one mg_decode_step = one pass of the whole hot path (SURVEY 8(a)
+rows a1-a11) over the batch.
 
 Three arms, each from the same deterministic prefill, W warm-up + K timed
 steps: tau = 0 (pure BF16, r_verify = 0), tau = tau_op (MarginGate, the
@@ -40,6 +43,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode tok/s + latency increment vs always-on verify; trigger %; determinism %"
+# calibration prompts (tau100) come from seeds CALIB_SEED + i, disjoint from the
+# evaluation seeds 7 + i of every rank at any world size
+CALIB_SEED = 10 ** 6
 
 
 def _peaks():
@@ -168,11 +174,15 @@ def run_gpu(args):
     shp = inputs.shape(args.model)
     B, K, W = args.batch, args.steps, args.warmup
     prompt_len, decode_len = inputs.WORKLOADS[args.workload]
-    ctx0 = prompt_len + decode_len // 2 - W        # timed steps sit at mid-decode context
+    ctx0 = max(prompt_len, prompt_len + decode_len - W - K)   # the timed steps end the decode
     max_seq = ctx0 + W + K + 2
     eng = Engine(shp, max_batch=B, max_slots=B, max_seq=max_seq, page_size=64)
     # requests of this rank: global ids rank*B .. rank*B + B-1 (request i -> rank i // B)
     prompts = inputs.prompts(B, ctx0, shp["vocab"], seed=7 + sharding.rank_requests(rank, ws, B)[0])
+    if ws > 1:
+        # cross-rank determinism probe: row 0 of every rank decodes
+        # global request 0 (protected), each time inside a different batch
+        prompts[0] = inputs.prompts(1, ctx0, shp["vocab"], seed=7)[0]
     out = torch.empty(B, dtype=torch.int32, device="cuda")
     kind = torch.empty(B, dtype=torch.uint8, device="cuda")
     stream = eng.stream
@@ -254,12 +264,12 @@ def run_gpu(args):
     prot_one, prot_all = inputs.protected_mask(B, "one"), inputs.protected_mask(B, "all")
     head = prot_one if args.protected == "one" else prot_all
     # operating threshold: the paper's protocol -- tau100
-    # calibrated on disjoint seeds (1000 + i) -- unless --tau fixes it; ranks
+    # calibrated on disjoint seeds (10^6 + i) -- unless --tau fixes it; ranks
     # agree on the largest (most conservative) value
     calib = None
     tau = args.tau
     if tau is None:
-        calib = calibrate(eng, inputs.prompts(B, ctx0, shp["vocab"], seed=1000 + rank * B), 3, min(K, 16))
+        calib = calibrate(eng, inputs.prompts(B, ctx0, shp["vocab"], seed=CALIB_SEED + rank * B), W, K)
         t100 = calib["tau100"] if calib["tau100"] is not None else math.inf
         _, (tau,) = sharding.aggregate([], [t100], device="cuda")
     res = {"bf16": run_arm(0.0, None)}
@@ -331,7 +341,7 @@ def run_gpu(args):
         if eng is not None:
             eng.close()
             eng = None
-        full = run_full_decode(args, pnames=("one",))
+        full = run_full_decode(args, pnames=("one", "all"))
 
     paper = None
     if not args.quick and args.paper_batch > 0:
@@ -339,7 +349,7 @@ def run_gpu(args):
             eng.close()
         pb = args.paper_batch
         e8 = Engine(shp, max_batch=pb, max_slots=pb, max_seq=ctx0 + W + max(K, 2 * args.window) + 2, page_size=64)
-        cal8 = calibrate(e8, inputs.prompts(pb, ctx0, shp["vocab"], seed=1000 + rank * pb), 3, K)
+        cal8 = calibrate(e8, inputs.prompts(pb, ctx0, shp["vocab"], seed=CALIB_SEED + rank * pb), 3, K)
         t8 = cal8["tau100"] if cal8["tau100"] is not None else math.inf
         _, (t8,) = sharding.aggregate([], [t8], device="cuda")
         ev8 = inputs.prompts(pb, ctx0, shp["vocab"], seed=7 + rank * pb)
@@ -371,9 +381,7 @@ def run_gpu(args):
 
     arms = [a for a in ("bf16", "mg", "ao", "ao_pipe", "mg_fused", "ao_fused", "mg_other", "ao_other", "ao_pipe_other",
                         "ao_fused_other") if a in res]
-    vec = []
-    for a in arms:
-        vec += [res[a]["stats"][k] for k in keys]
+
     def det_prefix(a, b, prot):  # pipelined rows may be shorter (a repair costs a step): common prefix
         ok = 0
         for i in range(B):
@@ -382,23 +390,24 @@ def run_gpu(args):
                 ok += res[a]["seqs"][i][:n] == res[b]["seqs"][i][:n]
         return ok, int(prot.sum())
 
-    dh = det("mg", "ao", head)
-    do = det("mg_other", "ao_other", prot_all if other == "all" else prot_one) if "mg_other" in res else (0, 0)
-    dp = det_prefix("ao_pipe", "ao", head)
-    df = det("mg_fused", "ao_fused", head)
-    vec += [*dh, *do, *dp, *df, *[res[a]["tokens"] for a in arms]]
-    times = [res[a]["ms"] for a in arms] + [e2e_ms]
-    vec, times = sharding.aggregate(vec, times, device="cuda")
+    dets = {"head": det("mg", "ao", head), "pipe": det_prefix("ao_pipe", "ao", head),
+            "fused": det("mg_fused", "ao_fused", head),
+            "other": det("mg_other", "ao_other", prot_all if other == "all" else prot_one) if "mg_other" in res
+            else (0, 0)}
+    times = {a: res[a]["ms"] for a in arms}
+    times["e2e"] = e2e_ms
+    red = sharding.reduce_run({a: res[a]["stats"] for a in arms}, keys, dets, {a: res[a]["tokens"] for a in arms},
+                              times, probe=res["mg"]["seqs"][0] if ws > 1 else None, device="cuda")
+    ao_probe = sharding.all_equal([sharding.digest(res["ao"]["seqs"][0])], device="cuda") if ws > 1 else None
     if rank != 0:
         if ws > 1:
             dist.destroy_process_group()
         return None
-    stats = {a: dict(zip(keys, vec[i * len(keys):(i + 1) * len(keys)])) for i, a in enumerate(arms)}
-    tail = vec[len(arms) * len(keys):]
-    dh, do, dp, df = tail[:2], tail[2:4], tail[4:6], tail[6:8]
-    ntok = dict(zip(arms, tail[8:]))
-    T = dict(zip(arms, times[:-1]))
-    t_e2e = times[-1]
+    stats = red["stats"]
+    dh, do, dp, df = red["det"]["head"], red["det"]["other"], red["det"]["pipe"], red["det"]["fused"]
+    ntok = red["tokens"]
+    T = {a: red["times"][a] for a in arms}
+    t_e2e = red["times"]["e2e"]
     tok = ws * B * K
 
     def summary(mg, ao, detv, prot_name):
@@ -434,7 +443,7 @@ def run_gpu(args):
                         "(tokens = emitted - replaced); determinism = common prefix equal to the sync always-on run"}
 
     arms_out = {"bf16_tok_s": round(tok / (T["bf16"] * 1e-3), 2), "tau": tau,
-                "tau_source": "calibrated tau100 (seeds 1000 + i)" if calib else "--tau",
+                "tau_source": "calibrated tau100 (seeds 10^6 + i)" if calib else "--tau",
                 "headline": summary("mg", "ao", dh, args.protected)}
     if calib:
         arms_out["calibration"] = calib
@@ -451,6 +460,7 @@ def run_gpu(args):
     if full is not None:
         arms_out["full_decode"] = {"workload": full["workload"], "calibration": full["calibration"],
                                    **full["arms"]["one"], "protected": "one",
+                                   "all_protected": full["arms"]["all"],
                                    "note": "rank 0; the whole decode, tau100 calibrated over the same length"}
     if w64 is not None:
         arms_out["llm42_window"] = {
@@ -460,10 +470,18 @@ def run_gpu(args):
             for p, v in w64.items()}
     if "mg_other" in res:
         arms_out["other"] = summary("mg_other", "ao_other", do, other)
+        if other == "all":   # determinism over every protected sequence of the batch (north star)
+            arms_out["determinism_all_protected"] = {
+                "margingate_pct": arms_out["other"]["determinism_pct"], "sequences": int(do[1]),
+                "reference": "always-on run of the same batch (= the batch-1 reference, tests/test_gpu_engine.py)"}
         arms_out["other"]["pipelined"] = pipe("ao_pipe_other", other, None)
         arms_out["other"]["fused"] = {
             "always_on_tok_s": round(tok / (T["ao_fused_other"] * 1e-3), 2),
             "inc_always_on": round(metrics.latency_increment(T["ao_fused_other"], T["bf16"]), 4)}
+    if ws > 1:
+        arms_out["cross_rank_determinism"] = {
+            "probe": "global request 0 decoded as row 0 (protected) on every rank, inside each rank's own batch",
+            "identical_on_all_ranks": {"margingate": red["probe_identical"], "always_on": ao_probe}}
     arms_out["paper_context"] = ("A6000, bs=8, one protected request: 2.23x (8B) / 1.99x (14B) increment reduction "
                                  "at 18.56% / 15.05% triggers (PAPER.md:5, 285, 296) -- context, not the target")
     line = {
@@ -479,8 +497,9 @@ def run_gpu(args):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights from the documented counter PRNG, uniform random prompts)",
-        "config": {"workload": f"{args.model}-shaped {args.workload} decode, batch {B}/GPU, "
-                               f"protected={args.protected}, tau={'tau100' if calib else tau}",
+        "config": {"workload": f"{args.model}-shaped {args.workload} decode, batch {B}/GPU, the last {K} decode "
+                               f"steps (contexts {ctx0 + W}..{ctx0 + W + K}), protected={args.protected}, "
+                               f"tau={'tau100' if calib else tau}",
                    "model": args.model, "global_batch": ws * B, "seq_len": ctx0 + W + K, "ctx_start": ctx0 + W,
                    "parallelism": f"request-sharded dp{ws}", "tau": tau, "protected": args.protected,
                    "l2": "inputs larger than L2 (15 GB of weights streamed per step)"},
@@ -582,24 +601,55 @@ def _verifier_roofline(shp, rows, ctx, ms, peak_gbs):
     return r
 
 
-def _oracle_sample(shp, prompt_len, steps, tau, budget_s):
-    """The oracle (as it stands) decoding one row: prefill `prompt_len` tokens
-    (untimed), then `steps` MarginGate decode steps at batch 1, timed."""
+def _oracle_sample(shp, prompt_len, steps, tau, budget_s, rows=1, sched_batch=1, model=None):
+    """The oracle (as it stands) decoding `rows` rows: prefill `prompt_len`
+    tokens (untimed), then up to `steps` MarginGate decode steps with the
+    oracle's batch-shaped plan of batch `sched_batch`, timed; returns (tokens,
+    seconds).  The oracle decodes rows independently, so a bounded sample of
+    rows of a large batch costs what those rows cost inside it."""
     import oracle
-    m = oracle.Model(shp)
-    p = [int(t) for t in np.random.default_rng(7).integers(0, shp["vocab"], prompt_len)]
-    st = oracle.State(m, 1, prompt_len + steps + 2)
+    m = model or oracle.Model(shp)
+    st = oracle.State(m, rows, prompt_len + steps + 2)
     det = oracle.det_sched()
-    st.prefill(0, p, det)
+    for r in range(rows):
+        st.prefill(r, [int(t) for t in np.random.default_rng(7 + r).integers(0, shp["vocab"], prompt_len)], det)
     t0 = time.time()
     n = 0
     for _ in range(steps):
-        st.step([0], [1], tau, oracle.fast_sched(1), det)
-        n += 1
+        st.step(list(range(rows)), [1] * rows, tau, oracle.fast_sched(sched_batch), det)
+        n += rows
         if time.time() - t0 > budget_s:
             break
     dt = time.time() - t0
     st.close()
+    if model is None:
+        m.close()
+    return n, dt
+
+
+def _oracle_tiny(bs, tau=0.3):
+    """BASELINE configs[0] in full: the tiny decoder, 8 prompts x 32 greedy
+    tokens, at batch 1 (each prompt alone) or batch 8; tokens/s of the timed
+    decode steps (prefill untimed)."""
+    import oracle
+
+    from paper_2605_30218_b200 import inputs
+    shp = inputs.shape("tiny")
+    m = oracle.Model(shp)
+    det = oracle.det_sched()
+    prompts = inputs.prompts(8, inputs.ragged_lengths(8, 8, 23), shp["vocab"])
+    n, dt = 0, 0.0
+    for g in range(0, 8, bs):
+        grp = prompts[g:g + bs]
+        st = oracle.State(m, len(grp), 64)
+        for i, p in enumerate(grp):
+            st.prefill(i, p, det)
+        t0 = time.time()
+        for _ in range(31):
+            st.step(list(range(len(grp))), [1] * len(grp), tau, oracle.fast_sched(len(grp)), det)
+        dt += time.time() - t0
+        n += 31 * len(grp)
+        st.close()
     m.close()
     return n, dt
 
@@ -618,10 +668,22 @@ def cpu_baseline(args, shp, tau):
     if avail and avail < need:
         return {"value": None, "unit": "tok/s", "cores": cores, "kind": "oracle",
                 "sample": f"skipped: {avail / 2**30:.0f} GiB host RAM < {need / 2**30:.0f} GiB needed"}
-    n, dt = _oracle_sample(shp, 8, 8, tau, 25.0)   # ~10-30 s of CPU work
-    return {"value": round(n / dt, 5), "unit": "tok/s", "cores": cores, "kind": "oracle",
-            "sample": f"{args.model}-shaped, 1 row, {n} MarginGate decode steps (tau={tau}) after an 8-token "
-                      f"deterministic prefill; {dt:.1f} s of CPU time"}
+    n, dt = _oracle_sample(shp, 8, 8, tau, 20.0)   # ~10-30 s of CPU work
+    out = {"value": round(n / dt, 5), "unit": "tok/s", "cores": cores, "kind": "oracle",
+           "sample": f"{args.model}-shaped, 1 row, {n} MarginGate decode steps (tau={tau}) after an 8-token "
+                     f"deterministic prefill; {dt:.1f} s of CPU time"}
+    # SURVEY 8(d) samples: the same model inside a batch of 64 (two rows of one
+    # step, the oracle's batch-64 reduction plan) and BASELINE configs[0] in full
+    n64, dt64 = _oracle_sample(shp, 8, 1, tau, 20.0, rows=2, sched_batch=64)
+    out["samples"] = {
+        f"{args.model}_bs64": {"value": round(n64 / dt64, 5), "unit": "tok/s",
+                               "sample": f"2 of the 64 rows of one step (batch-64 plan), {dt64:.1f} s"}}
+    for bs in (1, 8):
+        nt, dtt = _oracle_tiny(bs)
+        out["samples"][f"tiny_bs{bs}"] = {"value": round(nt / dtt, 2), "unit": "tok/s",
+                                          "sample": f"configs[0]: 8 prompts x 32 greedy tokens at batch {bs}, "
+                                                    f"tau 0.3, {dtt:.2f} s"}
+    return out
 
 
 def run_reference(args):
@@ -891,7 +953,7 @@ def run_sweep(args):
     B, K, W = args.batch, args.steps, args.warmup
     prompt_len, _ = inputs.WORKLOADS[args.workload]
     eng = Engine(shp, max_batch=B, max_slots=B, max_seq=prompt_len + W + K + 4, page_size=64)
-    cal = calibrate(eng, inputs.prompts(B, prompt_len, shp["vocab"], seed=1000), W, K)
+    cal = calibrate(eng, inputs.prompts(B, prompt_len, shp["vocab"], seed=CALIB_SEED), W, K)
     t_eval = cal["tau100"] if cal["tau100"] is not None else math.inf
     ev = inputs.prompts(B, prompt_len, shp["vocab"], seed=7)
     evals = {}
@@ -962,7 +1024,7 @@ def run_sweep(args):
     return {"metric": "tau calibration sweep (SURVEY 8(f) NEXT-1, A22)", "model": args.model,
             "hetero_check": het, "kv_deviation": kvd,
             "workload": f"{args.workload}-shaped prompt {prompt_len}, {K} timed decode steps after {W}, batch {B}",
-            "calibration": {"seeds": "1000 + i", **cal},
+            "calibration": {"seeds": "10^6 + i", **cal},
             "evaluation": {"seeds": "7 + i", **evals},
             "paper_context": "tab:pareto / tab:eps_pert (PAPER.md:260-265, 402-421): tau100 from a doubling "
                              "sweep on calibration prompts, A6000 -- context, not the target"}
@@ -973,7 +1035,7 @@ def run_full_decode(args, pnames=("one", "all"), eng=None):
     512 decode steps, SURVEY 8(d) "tok/s = emitted decode tokens / decode time"):
     contexts 128..640 cross the verifier's 512-key split, so the fast path's
     batch-shaped attention differs from the verifier in the second half.  tau100
-    calibrated over the same decode length on seeds 1000 + i; arms BF16,
+    calibrated over the same decode length on seeds 10^6 + i; arms BF16,
     MarginGate and always-on, synchronous and fused, one and all rows protected."""
     from paper_2605_30218_b200 import inputs, metrics
     from paper_2605_30218_b200.engine import Engine
@@ -985,7 +1047,7 @@ def run_full_decode(args, pnames=("one", "all"), eng=None):
     own = eng is None
     if own:
         eng = Engine(shp, max_batch=B, max_slots=B, max_seq=prompt_len + decode_len + 2, page_size=64)
-    cal = calibrate(eng, inputs.prompts(B, prompt_len, shp["vocab"], seed=1000), W, K)
+    cal = calibrate(eng, inputs.prompts(B, prompt_len, shp["vocab"], seed=CALIB_SEED), W, K)
     t100 = cal["tau100"] if cal["tau100"] is not None else math.inf
     ev = inputs.prompts(B, prompt_len, shp["vocab"], seed=7)
     out = {}
@@ -1016,7 +1078,7 @@ def run_full_decode(args, pnames=("one", "all"), eng=None):
 
 def run_batch_scaling(args):
     """tab:batch_scaling analog: latency increment over BF16
-    of MarginGate (tau100 calibrated per batch on seeds 1000 + i) and of
+    of MarginGate (tau100 calibrated per batch on seeds 10^6 + i) and of
     always-on verification, synchronous and fused verify modes, one protected
     request, at batch 8 / 16 / 32 / 64."""
     from paper_2605_30218_b200 import inputs, metrics
@@ -1029,7 +1091,7 @@ def run_batch_scaling(args):
     rows = []
     for B in (8, 16, 32, 64):
         eng = Engine(shp, max_batch=B, max_slots=B, max_seq=ctx0 + W + K + 2, page_size=64)
-        cal = calibrate(eng, inputs.prompts(B, ctx0, shp["vocab"], seed=1000), 3, min(K, 16))
+        cal = calibrate(eng, inputs.prompts(B, ctx0, shp["vocab"], seed=CALIB_SEED), 3, min(K, 16))
         t100 = cal["tau100"] if cal["tau100"] is not None else math.inf
         ev = inputs.prompts(B, ctx0, shp["vocab"], seed=7)
         p1 = inputs.protected_mask(B, "one")

@@ -19,10 +19,21 @@
  *    mg_query_sizes (e.g. with torch) and keeps them alive until mg_destroy.
  *    The context owns host metadata, CUDA events and tensor maps.
  *  - Synchrony: all work is ordered on the stream given to mg_init.
- *    mg_decode_step returns once the step is enqueued; it synchronises
- *    internally only to read the gate's trigger count when a protected row
- *    exists and 0 < tau (the verifier's token count is data dependent).
- *    Device outputs are valid after stream completion.  mg_stats synchronises.
+ *    mg_decode_step returns once the step is enqueued and never waits on the
+ *    device: in MG_VERIFY_SYNC the step is one CUDA graph whose verifier runs
+ *    behind device-side conditions (graph conditional nodes: WHILE over the
+ *    catch-up chunks, SWITCH on the chunk size, IF on the verifier's LM head)
+ *    set by the gate kernel.  Exceptions, all debug or first-use: the first
+ *    step of a new (batch, protected-count) shape and steps with logit
+ *    captures / timing / injected noise (include/mg_debug.h) run the same
+ *    kernels eagerly and read the gate back once.  Device outputs are valid
+ *    after stream completion.  mg_stats, mg_prefill and mg_verify_window
+ *    synchronise.
+ *  - Host arrays: the slots and the protection mask of a step are HOST
+ *    arrays (SURVEY 8(b) lists device pointers): the host owns the page
+ *    allocator and the capacity checks (MG_ERR_CAPACITY before any state
+ *    change), which need the slots without a device round trip; the mask
+ *    travels with the slots in the step's single H2D copy.
  *  - Threading: one context = one host thread.  Not thread-safe.
  *  - Arrays whose name ends in _host are host memory, _dev device memory.
  */
@@ -99,6 +110,13 @@ typedef enum { MG_REPAIR_COLUMN = 0, MG_REPAIR_TOKEN_ONLY = 1 } mg_repair_action
  *   MG_VERIFY_SYNC       the gated rows of a step are verified inside the same
  *                        mg_decode_step, before it commits;
  *                        every row's token is final when emitted; default.
+ *                        The verifier runs only when some protected row's gate
+ *                        fires; when it runs it catches up the
+ *                        shadow cache of EVERY protected row of the batch
+ *                        (its weight pass is paid anyway; results do not
+ *                        depend on the chunking, A23) and computes
+ *                        the LM head of every protected row -- only the fired
+ *                        rows commit the verifier token.
  *   MG_VERIFY_PIPELINED  a gated row's token is emitted TENTATIVELY (kind 3)
  *                        and verified in the slot's next step, whose forward
  *                        carries the verifier's catch-up tokens as extra GEMM
@@ -156,8 +174,8 @@ mg_status mg_prefill(mg_ctx* ctx, int32_t slot, const int32_t* prompt_host, int3
  *   margin_out_dev[b]      nullable: fp32 margin g of the fast logits
  * Each row consumes its last committed token at position p and commits exactly
  * one token.  MG_ERR_INVALID: batch not in [1, max_batch], inactive or
- * duplicate slot, tau NaN or < 0.  MG_ERR_CAPACITY: a row's p + 1 would reach
- * max_seq. */
+ * duplicate slot, tau NaN or < 0.  MG_ERR_CAPACITY: a row's position p has
+ * reached max_seq (columns are 0 .. max_seq - 1) or pages run out. */
 mg_status mg_decode_step(mg_ctx* ctx, const int32_t* slots_host, int32_t batch, const uint8_t* protected_host,
                          float threshold, int32_t* tokens_out_dev, uint8_t* kind_out_dev, float* margin_out_dev);
 

@@ -105,8 +105,10 @@ mg_status mgd_last_step(mg_ctx* ctx, int32_t* f_tok, float* g, float* v1, float*
 mg_status mgd_capture_logits(mg_ctx* ctx, float* dev_buf);
 
 /* From the next step on, after each verifier LM head copy the fp32 logits of
- * the gated rows into dev_buf[k][vocab], k = the row's rank among the step's
- * gated rows (ascending batch index); nullptr stops.  Disables CUDA graphs
+ * the verifier's rows into dev_buf[k][vocab], k = the row's rank among the
+ * rows the verifier ran on (ascending batch index): in MG_VERIFY_SYNC and
+ * MG_VERIFY_FUSED every protected row of a step whose verifier ran, in
+ * MG_VERIFY_PIPELINED the pending rows; nullptr stops.  Disables CUDA graphs
  * while set.  For the tau calibration (eps_pert). */
 mg_status mgd_capture_verifier_logits(mg_ctx* ctx, float* dev_buf);
 /* Copy the weight tensor (layer, which) as the ORACLE's logical layout

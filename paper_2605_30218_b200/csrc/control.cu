@@ -122,10 +122,13 @@ MG_DEV bool gate_fires(float g, float tau) { return tau > 0.f && (g < tau || isi
 __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
   griddep();
   __shared__ int wsum[32], wgap[32];
+  __shared__ int s_fired;
   const int b = threadIdx.x, warp = b >> 5, lane = b & 31;
   const bool valid = b < a.B;
   int slot = 0, p = 0, s0 = 0;
   bool tr = false;
+  if (b == 0) s_fired = 0;
+  __syncthreads();
   if (valid) {
     slot = a.slots[b];
     p = a.pos[slot];
@@ -135,6 +138,9 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
       p -= 1;
     } else if (a.list_protected) {  // fused verification: every protected row, before its margin exists
       tr = a.prot ? a.prot[b] != 0 : true;
+    } else if (a.eager) {  // synchronous: list every protected row, count the rows whose gate fires
+      tr = a.prot ? a.prot[b] != 0 : true;
+      if (tr && gate_fires(a.g[b], a.tau)) atomicAdd(&s_fired, 1);  // strict <
     } else {
       const bool prot = a.prot ? a.prot[b] != 0 : true;
       tr = prot && gate_fires(a.g[b], a.tau);  // strict <
@@ -159,8 +165,16 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
       wsum[w] = acc; wgap[w] = accg;
       acc += c; accg += cg;
     }
-    a.ctrl[0] = acc;   // number of gated rows
+    if (a.eager && s_fired == 0) accg = 0;  // nothing fired: no verifier this step
+    a.ctrl[0] = acc;   // number of listed rows
     a.ctrl[1] = accg;  // catch-up tokens M
+    if (a.eager) {
+      a.ran[0] = s_fired;
+      if (a.vctl) a.vctl[0] = 0;
+      if (a.h_loop) cudaGraphSetConditional(a.h_loop, accg > 0 ? 1u : 0u);
+      if (a.h_lm) cudaGraphSetConditional(a.h_lm, s_fired > 0 ? 1u : 0u);
+      if (a.h_lm && a.stats && s_fired > 0) atomicAdd(&a.stats[12], 1ull);
+    }
   }
   __syncthreads();
   if (!valid) return;
@@ -247,7 +261,7 @@ __global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
   const int b = blockIdx.x;
   const int slot = a.slots[b];
   const int p = a.pos[slot];
-  const bool listed = a.gate_ran && a.trig[b];
+  const bool listed = a.gate_ran && a.trig[b] && (!a.ran || a.ran[0] > 0);
   const bool tr = listed && (!a.spec || gate_fires(a.g[b], a.spec_tau));  // fused mode: the gate
   const int f = a.f_tok[b];
   const int v = tr ? a.v_tok[a.rank[b]] : -1;
@@ -277,7 +291,7 @@ __global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
     if (kind == 2) atomicAdd(&s[5], 1ull);
     if (b == 0) {
       atomicAdd(&s[0], 1ull);
-      if (a.gate_ran && a.ctrl[0] > 0) {
+      if (a.gate_ran && a.ctrl[0] > 0 && (!a.ran || a.ran[0] > 0)) {
         atomicAdd(&s[6], 1ull);
         atomicAdd(&s[7], (unsigned long long)a.ctrl[1]);
       }
@@ -287,6 +301,66 @@ __global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
 
 cudaError_t launch_commit(const CommitArgs& a, cudaStream_t st) {
   return launch_k(k_commit, dim3(a.B), dim3(256), 0, st, a);
+}
+
+// ------------------------------------------------------------------ device-side verifier dispatch
+__global__ void k_vchunk(VChunkArgs a) {
+  griddep();
+  __shared__ int s_n, s_base, s_tc;
+  if (threadIdx.x == 0) {
+    const int M = a.ctrl[1], c0 = a.vctl[0], rem = M - c0;
+    int k = a.n_sizes - 1;
+    for (int i = 0; i < a.n_sizes; ++i)
+      if (a.sizes[i] >= rem) { k = i; break; }
+    const int tc = a.sizes[k];
+    s_n = rem < tc ? rem : tc;
+    s_base = c0;
+    s_tc = tc;
+    a.vctl[1] = c0;
+    a.vctl[0] = c0 + tc;
+    if (a.stats) atomicAdd(&a.stats[11], 1ull);
+    if (a.h_case) cudaGraphSetConditional(a.h_case, (unsigned)k);
+    if (a.h_loop) cudaGraphSetConditional(a.h_loop, c0 + tc < M ? 1u : 0u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < s_tc; i += blockDim.x) {
+    if (i < s_n) {
+      const int e = s_base + i;
+      a.v_slot[i] = a.cu_slot[e];
+      a.v_pos[i] = a.cu_pos[e];
+      a.v_tok[i] = a.cu_tok[e];
+      a.v_nk[i] = a.cu_nk[e];
+    } else {  // no-op entry: no cache write (slot -1), no keys, a valid embedding row
+      a.v_slot[i] = -1;
+      a.v_pos[i] = 0;
+      a.v_tok[i] = 0;
+      a.v_nk[i] = 0;
+    }
+  }
+}
+
+cudaError_t launch_vchunk(const VChunkArgs& a, cudaStream_t st) {
+  if (a.n_sizes < 1 || a.n_sizes > 8) return cudaErrorInvalidValue;
+  return launch_k(k_vchunk, dim3(1), dim3(512), 0, st, a);
+}
+
+__global__ void k_gather_last(const uint16_t* __restrict__ xn, const int32_t* __restrict__ last,
+                              const int32_t* __restrict__ ctrl, const int32_t* __restrict__ vctl, int T, int d,
+                              uint16_t* __restrict__ xgn) {
+  griddep();
+  const int r = blockIdx.x;
+  if (r >= ctrl[0]) return;
+  const int l = last[r] - vctl[1];
+  if (l < 0 || l >= T) return;
+  const uint4* s = reinterpret_cast<const uint4*>(xn + (size_t)l * d);
+  uint4* o = reinterpret_cast<uint4*>(xgn + (size_t)r * d);
+  for (int j = threadIdx.x; j < d / 8; j += blockDim.x) o[j] = s[j];
+}
+
+cudaError_t launch_gather_last(const uint16_t* xn, const int32_t* last, const int32_t* ctrl, const int32_t* vctl,
+                               int T, int n_max, int d, uint16_t* xgn, cudaStream_t st) {
+  if (n_max <= 0) return cudaSuccess;
+  return launch_k(k_gather_last, dim3(n_max), dim3(128), 0, st, xn, last, ctrl, vctl, T, d, xgn);
 }
 
 // ------------------------------------------------------------------ window verify

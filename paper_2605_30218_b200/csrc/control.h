@@ -31,6 +31,21 @@ struct GateArgs {
   // fused same-step verification (MG_VERIFY_FUSED): list every protected row
   // (p = pos) before the fast forward, independent of the margin
   int32_t list_protected;
+  // synchronous verification with opportunistic eager catch-up
+  // (MG_VERIFY_SYNC): the trigger prot && g < tau decides WHETHER the verifier
+  // runs this step; when it runs it catches up EVERY protected row of the
+  // batch (the list is the protected rows, ascending; trig[] marks them),
+  // since its weight pass is paid anyway (A23: the verifier's
+  // results do not depend on the chunking).  ran[0] = rows whose gate fired;
+  // ctrl[1] = catch-up tokens if ran[0] > 0, else 0.
+  int32_t eager;
+  int32_t* ran;
+  // device-side dispatch (CUDA-graph conditional nodes): the loop over the
+  // catch-up chunks (WHILE) and the verifier's LM head (IF) run only when the
+  // gate fired; handles are 0 outside a graph.  vctl[0] (chunk cursor) is reset.
+  unsigned long long h_loop, h_lm;
+  int32_t* vctl;
+  unsigned long long* stats;  // [12] += 1 when the LM-head IF body runs (launch accounting)
 };
 cudaError_t launch_gate(const GateArgs& a, cudaStream_t st);
 
@@ -65,6 +80,9 @@ struct CommitArgs {
   // commit the verifier's result; all of them have their shadow cache caught up
   int spec;
   float spec_tau;
+  // MG_VERIFY_SYNC (eager catch-up): the listed rows were verified only if
+  // ran[0] > 0 (nullable: always)
+  const int32_t* ran;
   int32_t* tokens_out;
   uint8_t* kind_out;
   float* margin_out;
@@ -77,6 +95,27 @@ struct CommitArgs {
   int32_t* dbg_out;
 };
 cudaError_t launch_commit(const CommitArgs& a, cudaStream_t st);
+
+// one iteration of the synchronous verifier's chunk loop (device-side
+// dispatch): picks the smallest chunk size >= the remaining catch-up tokens
+// (the largest if none), writes the chunk's token list (entries past the end
+// are no-ops: slot -1, 0 keys), advances the cursor and sets the SWITCH
+// (chunk size) and WHILE (more chunks) conditions
+struct VChunkArgs {
+  const int32_t* ctrl;     // [1] = catch-up tokens M
+  int32_t* vctl;           // [0] cursor, [1] base of this chunk
+  const int32_t *cu_slot, *cu_pos, *cu_tok, *cu_nk;
+  int32_t *v_slot, *v_pos, *v_tok, *v_nk;
+  int32_t n_sizes;
+  int32_t sizes[8];        // ascending
+  unsigned long long h_loop, h_case;
+  unsigned long long* stats;  // [11] += 1 per iteration
+};
+cudaError_t launch_vchunk(const VChunkArgs& a, cudaStream_t st);
+// rows r < ctrl[0] whose last catch-up token lies in this chunk
+// (last[r] - vctl[1] in [0, T)): xgn[r] = xn[last[r] - vctl[1]]
+cudaError_t launch_gather_last(const uint16_t* xn, const int32_t* last, const int32_t* ctrl, const int32_t* vctl,
+                               int T, int n_max, int d, uint16_t* xgn, cudaStream_t st);
 
 // windowed verification (LLM-42 style)
 struct WindowArgs {

@@ -22,6 +22,8 @@
 #include <cstring>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/mg_debug.h"
 #include "engine.h"
 
@@ -33,6 +35,14 @@ constexpr int kSMs = 148;
 constexpr int kDetSplitKeys = 512;  // verifier attention: keys per split (A14)
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// NVTX ranges around the host phases of a step (SURVEY 4.6 / 5 tracing): a
+// profiler (nsys, ncu --nvtx) attributes the enqueued kernels to fast / gate /
+// verify / commit.  Header-only NVTX v3: no cost without a tool attached.
+struct Nvtx {
+  explicit Nvtx(const char* m) { nvtxRangePushA(m); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 struct Carver {
   char* base;
@@ -293,6 +303,10 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
     const size_t a4 = 4 * (size_t)B, b2 = 2 * (size_t)c->max_pages;
     c->staging_d = s.take<int32_t>((a4 > b2 ? a4 : b2) + 64);
   }
+  c->vx_slot = s.take<int32_t>(Tm); c->vx_pos = s.take<int32_t>(Tm);
+  c->vx_tok = s.take<int32_t>(Tm); c->vx_nk = s.take<int32_t>(Tm);
+  c->vctl_d = s.take<int32_t>(4);
+  c->ran_d = s.take<int32_t>(4);
   c->dbg_vtok = s.take<int32_t>(B); c->dbg_out = s.take<int32_t>(B);
   c->dbg_vg = s.take<float>(B);
   c->dbg_kind = s.take<uint8_t>(B); c->dbg_trig = s.take<uint8_t>(B);
@@ -747,6 +761,7 @@ static void mark_pending_list_dirty(mg_ctx* c) {
 
 static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const uint8_t* prot, float tau,
                                   int32_t* tokens_out, uint8_t* kind_out, float* margin_out) {
+  Nvtx step_range("mg.step.pipelined");
   mg_status r = pipe_refresh(c);
   if (r) return r;
   const int S = c->cfg.max_slots;
@@ -915,6 +930,7 @@ static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const 
 // synchronous mode; the host never waits on the device inside a step.
 static mg_status decode_fused(mg_ctx* c, const int32_t* slots, int B, const uint8_t* prot, float tau,
                               int32_t* tokens_out, uint8_t* kind_out, float* margin_out) {
+  Nvtx step_range("mg.step.fused");
   const int S = c->cfg.max_slots;
   std::vector<char> seen(S, 0);
   int max_ctx = 1, need_pages = 0;
@@ -1044,6 +1060,315 @@ static mg_status decode_fused(mg_ctx* c, const int32_t* slots, int B, const uint
   return MG_OK;
 }
 
+// ---- synchronous verification (MG_VERIFY_SYNC) -------------------------
+// Semantics: the gate prot && g < tau picks the
+// rows whose verifier token is committed; the verifier runs only when some
+// row fires.  When it runs it catches up EVERY protected row of the batch
+// (shadow_len..p), not only the fired ones: its weight pass is paid anyway,
+// and the results do not depend on the chunking (A23), so the
+// committed tokens are those of the lazy form while no protected row's gap
+// can grow past one step of verifier activity (with every row protected
+// MarginGate never costs more than always-on verification).
+//
+// Dispatch: one CUDA graph per step shape -- fast forward + LM head + top-2,
+// the gate (which sets two graph conditions), a WHILE node over the catch-up
+// chunks whose body picks the chunk size with a SWITCH node (k_vchunk), an IF
+// node with the verifier's LM head, and the commit.  The host never waits on
+// the device inside a step.  The debug modes (logit captures, timing,
+// injected noise) and the first use of a shape run the same kernels eagerly
+// with one host readback of the gate.
+
+// chunk sizes of the verifier loop: powers of two from 16 up to the verify
+// chunk, within the activation rows
+static std::vector<int> vchunk_sizes(const mg_ctx* c) {
+  const int cap = std::min(c->Tmax, std::max(c->Tv, 16));
+  std::vector<int> v;
+  for (int t = 16; t <= 512 && t <= cap; t *= 2) v.push_back(t);
+  if (v.empty()) v.push_back(cap);
+  return v;
+}
+
+static GateArgs sync_gate_args(mg_ctx* c, int B, float tau) {
+  GateArgs ga{};
+  ga.g = c->f_g; ga.prot = c->prot_d; ga.tau = tau; ga.slots = c->slots_d; ga.B = B;
+  ga.pos = c->pos_d; ga.shadow_len = c->shadow_d; ga.hist = c->hist_d; ga.hist_stride = c->cfg.max_seq + 1;
+  ga.trig = c->trig_d; ga.rank = c->rank_d; ga.ctrl = c->ctrl_d; ga.last = c->last_d;
+  ga.cu_slot = c->cu_slot; ga.cu_pos = c->cu_pos; ga.cu_tok = c->cu_tok; ga.cu_nk = c->cu_nk;
+  ga.eager = 1; ga.ran = c->ran_d; ga.vctl = c->vctl_d;
+  return ga;
+}
+
+static CommitArgs sync_commit_args(mg_ctx* c, int B, float tau, bool gate, int32_t* tokens_out, uint8_t* kind_out,
+                                   float* margin_out) {
+  CommitArgs ca{};
+  ca.B = B; ca.slots = c->slots_d; ca.prot = c->prot_d; ca.gate_ran = gate ? 1 : 0; ca.trig = c->trig_d;
+  ca.rank = c->rank_d; ca.ctrl = c->ctrl_d; ca.f_tok = c->f_tok; ca.g = c->f_g; ca.v_tok = c->v_tok; ca.v_g = c->v_g;
+  ca.pos = c->pos_d; ca.shadow_len = c->shadow_d; ca.hist = c->hist_d; ca.hist_stride = c->cfg.max_seq + 1;
+  ca.copy = col_copy(c, true);
+  ca.repair_copy = c->repair_mode == MG_REPAIR_COLUMN ? 1 : 0;
+  ca.spec = 1; ca.spec_tau = tau;  // listed = protected; the gate picks the committed verifier tokens
+  ca.ran = gate ? c->ran_d : nullptr;
+  ca.tokens_out = tokens_out; ca.kind_out = kind_out; ca.margin_out = margin_out; ca.stats = c->stats_d;
+  ca.dbg_vtok = c->dbg_vtok; ca.dbg_vg = c->dbg_vg; ca.dbg_kind = c->dbg_kind; ca.dbg_trig = c->dbg_trig;
+  ca.dbg_out = c->dbg_out;
+  return ca;
+}
+
+// the fast forward + LM head + top-2 of B rows (fast cache, batch-shaped plan)
+static mg_status fast_pass(mg_ctx* c, int B, const Sched& fs) {
+  CK(launch_prepare(c->slots_d, B, c->pos_d, c->hist_d, c->cfg.max_seq + 1, c->f_slot, c->f_pos, c->f_tok,
+                    c->f_nk, c->st));
+  c->launches++;
+  mg_status rr = forward(c, B, c->f_slot, c->f_pos, c->f_tok, c->f_nk, 0, fs);
+  if (rr) return rr;
+  return lm_head(c, c->xn, c->Tmax, B, fs.lm, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g, c->f_slot, c->f_pos);
+}
+
+// add a conditional node after the capture's current dependencies
+static cudaError_t add_cond_node(cudaStream_t st, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type,
+                                 unsigned size, cudaGraph_t* bodies) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps;
+  size_t nd;
+  cudaError_t e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd);
+  if (e) return e;
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = type;
+  p.conditional.size = size;
+  cudaGraphNode_t node;
+  if ((e = cudaGraphAddNode(&node, g, deps, nd, &p))) return e;
+  if ((e = cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies))) return e;
+  for (unsigned i = 0; i < size; ++i) bodies[i] = p.conditional.phGraph_out[i];
+  return cudaSuccess;
+}
+
+// capture `body` (launches on c->st) into the conditional body graph g
+template <class F>
+static mg_status capture_body(mg_ctx* c, cudaGraph_t g, F&& body) {
+  cudaStream_t saved = c->st;
+  CK(cudaStreamBeginCaptureToGraph(c->cap_st2, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  c->st = c->cap_st2;
+  mg_status r = body();
+  c->st = saved;
+  cudaGraph_t out = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->cap_st2, &out);
+  if (r) return r;
+  CK(e);
+  return MG_OK;
+}
+
+static mg_status build_sync_graph(mg_ctx* c, int B, int n_lm, float tau, const Sched& fs, int32_t* tokens_out,
+                                  uint8_t* kind_out, float* margin_out, cudaGraphExec_t* out,
+                                  unsigned long long* fixed_launches) {
+  if (!c->cap_st) CK(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking));
+  if (!c->cap_st2) CK(cudaStreamCreateWithFlags(&c->cap_st2, cudaStreamNonBlocking));
+  const std::vector<int> sizes = vchunk_sizes(c);
+  const int nsz = (int)sizes.size();
+  cudaStream_t user = c->st;
+  const unsigned long long l0 = c->launches;
+  CK(cudaStreamBeginCapture(c->cap_st, cudaStreamCaptureModeThreadLocal));
+  c->st = c->cap_st;
+  mg_status r = MG_OK;
+  cudaGraph_t graph = nullptr;
+  auto body = [&]() -> mg_status {
+    mg_status rr = fast_pass(c, B, fs);
+    if (rr) return rr;
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g;
+    CK(cudaStreamGetCaptureInfo(c->st, &cs, nullptr, &g, nullptr, nullptr));
+    cudaGraphConditionalHandle h_loop, h_lm;
+    CK(cudaGraphConditionalHandleCreate(&h_loop, g, 0, cudaGraphCondAssignDefault));
+    CK(cudaGraphConditionalHandleCreate(&h_lm, g, 0, cudaGraphCondAssignDefault));
+    GateArgs ga = sync_gate_args(c, B, tau);
+    ga.h_loop = h_loop;
+    ga.h_lm = h_lm;
+    ga.stats = c->stats_d;
+    CK(launch_gate(ga, c->st));
+    c->launches++;
+    // WHILE (catch-up tokens left): k_vchunk, then SWITCH over the chunk sizes
+    cudaGraph_t wbody;
+    CK(add_cond_node(c->st, h_loop, cudaGraphCondTypeWhile, 1, &wbody));
+    cudaGraphConditionalHandle h_case;
+    CK(cudaGraphConditionalHandleCreate(&h_case, wbody, 0, cudaGraphCondAssignDefault));
+    cudaGraph_t cases[8];
+    const unsigned long long lb0 = c->launches;
+    rr = capture_body(c, wbody, [&]() -> mg_status {
+      VChunkArgs va{};
+      va.ctrl = c->ctrl_d; va.vctl = c->vctl_d;
+      va.cu_slot = c->cu_slot; va.cu_pos = c->cu_pos; va.cu_tok = c->cu_tok; va.cu_nk = c->cu_nk;
+      va.v_slot = c->vx_slot; va.v_pos = c->vx_pos; va.v_tok = c->vx_tok; va.v_nk = c->vx_nk;
+      va.n_sizes = nsz;
+      for (int i = 0; i < nsz; ++i) va.sizes[i] = sizes[i];
+      va.h_loop = h_loop; va.h_case = h_case; va.stats = c->stats_d;
+      CK(launch_vchunk(va, c->st));
+      c->launches++;
+      CK(add_cond_node(c->st, h_case, cudaGraphCondTypeSwitch, (unsigned)nsz, cases));
+      return MG_OK;
+    });
+    if (rr) return rr;
+    for (int k = 0; k < nsz; ++k) {
+      const unsigned long long lk = c->launches;
+      rr = capture_body(c, cases[k], [&]() -> mg_status {
+        const int T = sizes[k];
+        Sched sc = sched_det(c, T, c->cfg.max_seq);  // splits sized from the capacity: one graph per decode
+        mg_status q = forward(c, T, c->vx_slot, c->vx_pos, c->vx_tok, c->vx_nk, 1, sc);
+        if (q) return q;
+        CK(launch_gather_last(c->xn, c->last_d, c->ctrl_d, c->vctl_d, T, B, c->d, c->xgn, c->st));
+        c->launches++;
+        return MG_OK;
+      });
+      if (rr) return rr;
+      if (k > 0) c->launches = lk;  // every case launches the same kernels: count one
+    }
+    c->cond_body_launches = c->launches - lb0;
+    c->launches = lb0;
+    // IF (some row fired): the verifier's LM head + top-2 over the listed rows
+    cudaGraph_t lbody;
+    CK(add_cond_node(c->st, h_lm, cudaGraphCondTypeIf, 1, &lbody));
+    const unsigned long long ll0 = c->launches;
+    rr = capture_body(c, lbody, [&]() -> mg_status {
+      return lm_head(c, c->xgn, c->cfg.max_batch, n_lm, op_lm(c->V, c->d, n_lm, true), c->v_v1, c->v_tok, c->v_v2,
+                     c->v_i2, c->v_g);
+    });
+    if (rr) return rr;
+    c->cond_lm_launches = c->launches - ll0;
+    c->launches = ll0;
+    CommitArgs ca = sync_commit_args(c, B, tau, true, tokens_out, kind_out, margin_out);
+    CK(launch_commit(ca, c->st));
+    c->launches++;
+    return MG_OK;
+  };
+  r = body();
+  c->st = user;
+  cudaError_t e = cudaStreamEndCapture(c->cap_st, &graph);
+  if (r) {
+    if (graph) cudaGraphDestroy(graph);
+    return r;
+  }
+  CK(e);
+  e = cudaGraphInstantiate(out, graph, 0);
+  cudaGraphDestroy(graph);
+  CK(e);
+  *fixed_launches = c->launches - l0;
+  c->launches = l0;
+  return MG_OK;
+}
+
+static mg_status refresh_shadow(mg_ctx* c) {
+  if (!c->shadow_stale) return MG_OK;
+  std::vector<int32_t> sh(c->cfg.max_slots);
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaMemcpy(sh.data(), c->shadow_d, sh.size() * 4, cudaMemcpyDeviceToHost));
+  for (int s = 0; s < c->cfg.max_slots; ++s)
+    if (c->active[s]) c->shadow_h[s] = sh[s];
+  c->shadow_stale = false;
+  return MG_OK;
+}
+
+static mg_status decode_sync(mg_ctx* c, const int32_t* slots, int B, const uint8_t* prot, float tau,
+                             int32_t* tokens_out, uint8_t* kind_out, float* margin_out) {
+  Nvtx step_range("mg.step.sync");
+  std::vector<char> seen(c->cfg.max_slots, 0);
+  int max_ctx = 1, need_pages = 0, n_prot = 0;
+  for (int b = 0; b < B; ++b) {
+    const int s = slots[b];
+    if (s < 0 || s >= c->cfg.max_slots || !c->active[s] || seen[s])
+      return fail(c, MG_ERR_INVALID, "inactive or duplicate slot");
+    seen[s] = 1;
+    const int p = c->pos_h[s];
+    if (p >= c->cfg.max_seq) return fail(c, MG_ERR_CAPACITY, "max_seq reached");
+    if (p / c->PS >= (int)c->pages[s].size()) ++need_pages;
+    if (p + 1 > max_ctx) max_ctx = p + 1;
+    if (!prot || prot[b]) ++n_prot;
+  }
+  if ((int)c->free_pages.size() < need_pages) return fail(c, MG_ERR_CAPACITY, "KV pages exhausted");
+  size_t ev0 = 0;
+  if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
+  mg_status r = upload_batch(c, slots, B, prot);  // one H2D copy: slots, mask, page-table entries
+  if (r) return r;
+  const bool gate = n_prot > 0 && tau > 0.f;
+  Sched fs = sched_fast(c, B, max_ctx);
+  const int fkey = fs.qkv.impl * 4096 + fs.qkv.mma_n * 8 + (c->lm_unfused ? 1 : 0);
+  const bool debug = !c->use_graphs || c->timing.on || c->capture || c->capture_v || c->inj_amp > 0.f;
+  int n_lm = 1;
+  while (n_lm < n_prot) n_lm <<= 1;
+  if (n_lm > B) n_lm = B;  // LM rows: power-of-two bucket (rows past n_prot repeat nothing and are unused)
+  bool done = false;
+  if (gate && !debug) {
+    auto& g = c->graphs[std::make_tuple(5, B, fs.attn_ns, fs.attn_sk, n_lm,
+                                        (c->fast_mode * 2 + c->repair_mode) * 65536 + fkey)];
+    if (!g.exec && ++g.seen >= 2) {
+      unsigned long long fixed = 0;
+      if ((r = build_sync_graph(c, B, n_lm, tau, fs, tokens_out, kind_out, margin_out, &g.exec, &fixed))) return r;
+      g.launches = fixed;
+    }
+    if (g.exec) {
+      Nvtx gr("mg.step.graph (fast | gate | verify | commit)");
+      // the outputs and tau are baked into the graph: rebuild when they change
+      if (g.tok != tokens_out || g.kind != kind_out || g.marg != margin_out || g.tau != tau) {
+        cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+        unsigned long long fixed = 0;
+        if ((r = build_sync_graph(c, B, n_lm, tau, fs, tokens_out, kind_out, margin_out, &g.exec, &fixed))) return r;
+        g.launches = fixed;
+      }
+      g.tok = tokens_out; g.kind = kind_out; g.marg = margin_out; g.tau = tau;
+      CK(cudaGraphLaunch(g.exec, c->st));
+      c->launches += g.launches;
+      c->shadow_stale = true;
+      done = true;
+    }
+  }
+  if (!done) {
+    // eager form: the same kernels, one host readback of the gate
+    {
+      Nvtx fr("mg.fast");
+      r = graphed(c, std::make_tuple(0, B, fs.attn_ns, fs.attn_sk, c->fast_mode, fkey),
+                  [&]() -> mg_status { return fast_pass(c, B, fs); });
+      if (r) return r;
+    }
+    if (c->capture) CK(cudaMemcpyAsync(c->capture, c->logits, (size_t)B * c->V * 4, cudaMemcpyDeviceToDevice, c->st));
+    int ran = 0, n_list = 0;
+    if (gate) {
+      Nvtx gr("mg.gate+verify");
+      GateArgs ga = sync_gate_args(c, B, tau);
+      CK(launch_gate(ga, c->st));
+      c->launches++;
+      const int MB = c->cfg.max_batch;
+      int32_t* h = c->spin;  // [ctrl: 2 + MB] [last: MB] [ran]
+      CK(cudaMemcpyAsync(h, c->ctrl_d, (2 + B) * 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(h + 2 + MB, c->last_d, B * 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(h + 2 + 2 * MB, c->ran_d, 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      n_list = h[0];
+      const int M = h[1];
+      ran = h[2 + 2 * MB];
+      if (n_list != n_prot) return fail(c, MG_ERR_CUDA, "protected-row count mismatch between host and device");
+      if (M > 0) {
+        std::vector<int> last(h + 2 + MB, h + 2 + MB + n_list);
+        if ((r = run_det(c, M, last, c->cfg.max_seq))) return r;
+      }
+    }
+    Nvtx cr("mg.commit");
+    CommitArgs ca = sync_commit_args(c, B, tau, gate, tokens_out, kind_out, margin_out);
+    CK(launch_commit(ca, c->st));
+    c->launches++;
+    if (ran > 0 && !c->shadow_stale)
+      for (int b = 0; b < B; ++b)
+        if (!prot || prot[b]) c->shadow_h[slots[b]] = c->pos_h[slots[b]] + 1;
+  }
+  if (c->timing.on) {
+    cudaEventRecord(tevent(c), c->st);
+    c->timing.rec.emplace_back(ev0, c->timing.used - 1, 2, 0.0);
+  }
+  for (int b = 0; b < B; ++b) c->pos_h[slots[b]] += 1;
+  c->last_B = B;
+  return MG_OK;
+}
+
 static std::string g_init_err;
 
 extern "C" {
@@ -1125,7 +1450,8 @@ mg_status mg_init(const mg_config* cfg, const mg_buffers* bufs, void* stream, mg
     const char* fs = getenv("MG_FAST_SK");  // measurement knobs: attention split sizes
     c->fast_sk_override = fs ? atoi(fs) : 0;
   }
-  if ((e = cudaMallocHost(&c->fpin, fpin_words(c) * 4)) || (e = cudaEventCreateWithFlags(&c->fev, cudaEventDisableTiming)))
+  if ((e = cudaMallocHost(&c->fpin, fpin_words(c) * 4)) || (e = cudaEventCreateWithFlags(&c->fev, cudaEventDisableTiming)) ||
+      (e = cudaMallocHost(&c->spin, (4 + 2 * (size_t)c->cfg.max_batch) * 4)))
     return die(cudaGetErrorString(e));
   memset(c->fpin, 0, fpin_words(c) * 4);
   c->pend_h.assign(c->cfg.max_slots, 0);
@@ -1140,6 +1466,7 @@ mg_status mg_init(const mg_config* cfg, const mg_buffers* bufs, void* stream, mg
 
 mg_status mg_prefill(mg_ctx* c, int32_t slot, const int32_t* prompt, int32_t len, int32_t* first_token) {
   if (!c) return MG_ERR_INVALID;
+  Nvtx range("mg.prefill");
   if (c->dead) return fail(c, MG_ERR_CUDA, "context is dead: " + c->err);
   if (slot < 0 || slot >= c->cfg.max_slots || !prompt || len < 1 || !first_token)
     return fail(c, MG_ERR_INVALID, "bad prefill arguments");
@@ -1189,105 +1516,7 @@ mg_status mg_decode_step(mg_ctx* c, const int32_t* slots, int32_t B, const uint8
   if (c->verify_mode == MG_VERIFY_PIPELINED)
     return decode_pipelined(c, slots, B, prot, tau, tokens_out, kind_out, margin_out);
   if (c->verify_mode == MG_VERIFY_FUSED) return decode_fused(c, slots, B, prot, tau, tokens_out, kind_out, margin_out);
-  std::vector<char> seen(c->cfg.max_slots, 0);
-  int max_ctx = 1;
-  int need_pages = 0;
-  bool any_prot = false;
-  for (int b = 0; b < B; ++b) {
-    const int s = slots[b];
-    if (s < 0 || s >= c->cfg.max_slots || !c->active[s] || seen[s])
-      return fail(c, MG_ERR_INVALID, "inactive or duplicate slot");
-    seen[s] = 1;
-    const int p = c->pos_h[s];
-    if (p >= c->cfg.max_seq) return fail(c, MG_ERR_CAPACITY, "max_seq reached");
-    if (p / c->PS >= (int)c->pages[s].size()) ++need_pages;
-    if (p + 1 > max_ctx) max_ctx = p + 1;
-    if (!prot || prot[b]) any_prot = true;
-  }
-  if ((int)c->free_pages.size() < need_pages) return fail(c, MG_ERR_CAPACITY, "KV pages exhausted");
-  size_t ev0 = 0;
-  if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
-
-  // 1. upload batch + page-table updates (one H2D copy)
-  {
-    mg_status r = upload_batch(c, slots, B, prot);
-    if (r) return r;
-  }
-  // 2. fast path (one CUDA graph per (B, attention splits))
-  Sched fs = sched_fast(c, B, max_ctx);
-  // key: everything the captured launch sequence depends on (schedule mode,
-  // GEMM engine and MMA width, attention splits)
-  mg_status r = graphed(c, std::make_tuple(0, B, fs.attn_ns, fs.attn_sk, c->fast_mode,
-                                           fs.qkv.impl * 4096 + fs.qkv.mma_n * 8 + (c->lm_unfused ? 1 : 0)),
-                        [&]() -> mg_status {
-    CK(launch_prepare(c->slots_d, B, c->pos_d, c->hist_d, c->cfg.max_seq + 1, c->f_slot, c->f_pos, c->f_tok,
-                      c->f_nk, c->st));
-    c->launches++;
-    mg_status rr = forward(c, B, c->f_slot, c->f_pos, c->f_tok, c->f_nk, 0, fs);
-    if (rr) return rr;
-    return lm_head(c, c->xn, c->Tmax, B, fs.lm, c->f_v1, c->f_tok, c->f_v2, c->f_i2, c->f_g, c->f_slot, c->f_pos);
-  });
-  if (r) return r;
-  if (c->capture) CK(cudaMemcpyAsync(c->capture, c->logits, (size_t)B * c->V * 4, cudaMemcpyDeviceToDevice, c->st));
-
-  // 3. gate (+ 4. verifier)
-  const bool gate = any_prot && tau > 0.f;
-  int n_gated = 0;
-  std::vector<int> rows;
-  if (gate) {
-    GateArgs ga{};
-    ga.g = c->f_g; ga.prot = c->prot_d; ga.tau = tau; ga.slots = c->slots_d; ga.B = B;
-    ga.pos = c->pos_d; ga.shadow_len = c->shadow_d; ga.hist = c->hist_d; ga.hist_stride = c->cfg.max_seq + 1;
-    ga.trig = c->trig_d; ga.rank = c->rank_d; ga.ctrl = c->ctrl_d; ga.last = c->last_d;
-    ga.cu_slot = c->cu_slot; ga.cu_pos = c->cu_pos; ga.cu_tok = c->cu_tok; ga.cu_nk = c->cu_nk;
-    CK(launch_gate(ga, c->st));
-    c->launches++;
-    int32_t* ctrl_h = c->pinned + (c->pinned_words - (2 + c->cfg.max_batch));
-    CK(cudaMemcpyAsync(ctrl_h, c->ctrl_d, (2 + B) * 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    n_gated = ctrl_h[0];
-    const int M = ctrl_h[1];
-    rows.assign(ctrl_h + 2, ctrl_h + 2 + n_gated);
-    if (n_gated > 0) {
-      std::vector<int> last;
-      int off = 0, vmax = 1;
-      for (int i = 0; i < n_gated; ++i) {
-        const int s = slots[rows[i]];
-        const int gap = c->pos_h[s] - c->shadow_h[s] + 1;
-        off += gap;
-        last.push_back(off - 1);
-        if (c->pos_h[s] + 1 > vmax) vmax = c->pos_h[s] + 1;
-      }
-      if (off != M) return fail(c, MG_ERR_CUDA, "catch-up size mismatch between host mirror and device");
-      if ((r = run_det(c, M, last, vmax))) return r;
-    }
-  }
-  // 5. commit
-  CommitArgs ca{};
-  ca.B = B; ca.slots = c->slots_d; ca.prot = c->prot_d; ca.gate_ran = gate ? 1 : 0; ca.trig = c->trig_d;
-  ca.rank = c->rank_d; ca.ctrl = c->ctrl_d; ca.f_tok = c->f_tok; ca.g = c->f_g; ca.v_tok = c->v_tok; ca.v_g = c->v_g;
-  ca.pos = c->pos_d; ca.shadow_len = c->shadow_d; ca.hist = c->hist_d; ca.hist_stride = c->cfg.max_seq + 1;
-  ca.copy = col_copy(c, true);
-  ca.repair_copy = c->repair_mode == MG_REPAIR_COLUMN ? 1 : 0;
-  ca.tokens_out = tokens_out; ca.kind_out = kind_out; ca.margin_out = margin_out; ca.stats = c->stats_d;
-  ca.dbg_vtok = c->dbg_vtok; ca.dbg_vg = c->dbg_vg; ca.dbg_kind = c->dbg_kind; ca.dbg_trig = c->dbg_trig;
-  ca.dbg_out = c->dbg_out;
-  CK(launch_commit(ca, c->st));
-  c->launches++;
-  if (c->timing.on) {
-    cudaEventRecord(tevent(c), c->st);
-    c->timing.rec.emplace_back(ev0, c->timing.used - 1, 2, 0.0);
-  }
-  for (int b = 0; b < B; ++b) {
-    const int s = slots[b];
-    c->pos_h[s] += 1;
-  }
-  for (int i = 0; i < n_gated; ++i) {
-    const int s = slots[rows[i]];
-    c->shadow_h[s] = c->pos_h[s];
-  }
-  c->last_B = B;
-  return MG_OK;
+  return decode_sync(c, slots, B, prot, tau, tokens_out, kind_out, margin_out);
 }
 
 mg_status mg_set_policy(mg_ctx* c, int32_t fast_schedule, int32_t repair_action, int32_t verify_mode) {
@@ -1301,6 +1530,7 @@ mg_status mg_set_policy(mg_ctx* c, int32_t fast_schedule, int32_t repair_action,
     return fail(c, MG_ERR_INVALID, "unknown verify mode");
   mg_status r = pipe_refresh(c);
   if (r) return r;
+  if ((r = refresh_shadow(c))) return r;
   if (verify_mode != c->verify_mode)
     for (int s = 0; s < c->cfg.max_slots; ++s)
       if (c->active[s] && c->pend_h[s])
@@ -1319,6 +1549,7 @@ mg_status mg_verify_window(mg_ctx* c, const int32_t* slots, int32_t n, int32_t* 
   if (!slots || n < 1 || n > c->cfg.max_batch) return fail(c, MG_ERR_INVALID, "bad window batch");
   mg_status rf = pipe_refresh(c);
   if (rf) return rf;
+  if ((rf = refresh_shadow(c))) return rf;
   std::vector<char> seen(c->cfg.max_slots, 0);
   for (int i = 0; i < n; ++i) {
     const int s = slots[i];
@@ -1433,6 +1664,8 @@ void mg_destroy(mg_ctx* c) {
   if (c->stage_ev[1]) cudaEventDestroy(c->stage_ev[1]);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->fpin) cudaFreeHost(c->fpin);
+  if (c->spin) cudaFreeHost(c->spin);
+  if (c->cap_st2) cudaStreamDestroy(c->cap_st2);
   if (c->fev) cudaEventDestroy(c->fev);
   delete c;
 }
@@ -1460,6 +1693,7 @@ mg_status mgd_read_column(mg_ctx* c, int32_t which, int32_t slot, int32_t pos, u
 
 mg_status mgd_cache_digest(mg_ctx* c, int32_t which, int32_t skip_slot, int32_t skip_pos, uint64_t* out) {
   if (!c || !out) return MG_ERR_INVALID;
+  if (mg_status r = refresh_shadow(c)) return r;
   uint64_t h = 1469598103934665603ull;
   std::vector<uint16_t> col((size_t)c->L * 2 * c->KV * c->hd);
   for (int s = 0; s < c->cfg.max_slots; ++s) {
@@ -1579,7 +1813,13 @@ mg_status mgd_force_schedule(mg_ctx* c, int32_t B_as_if) {
 
 mg_status mgd_launch_count(mg_ctx* c, uint64_t* out) {
   if (!c || !out) return MG_ERR_INVALID;
-  *out = c->launches;
+  // kernels inside conditional graph nodes run only when the device says so:
+  // counted from the device's iteration counters (stats[11] loop bodies,
+  // stats[12] verifier LM heads of graph-dispatched steps)
+  unsigned long long s[16];
+  CK(cudaMemcpyAsync(s, c->stats_d, sizeof(s), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  *out = c->launches + s[11] * c->cond_body_launches + s[12] * c->cond_lm_launches;
   return MG_OK;
 }
 

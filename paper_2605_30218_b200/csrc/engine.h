@@ -132,7 +132,7 @@ struct mg_ctx {
   int stage_idx = 0;
 
   std::map<std::tuple<const void*, int, int, int>, CUtensorMap> xmaps;
-  unsigned long long launches = 0;
+  unsigned long long launches = 0;   // kernels enqueued (conditional bodies: mgd_launch_count adds them)
   mg::Timing timing;
 
   // CUDA graphs of the launch sequences (fast step per (B, attention chunks);
@@ -141,8 +141,20 @@ struct mg_ctx {
     cudaGraphExec_t exec = nullptr;
     int seen = 0;
     unsigned long long launches = 0;
+    // whole-step graphs (decode_sync) bake in the outputs and the threshold
+    const void *tok = nullptr, *kind = nullptr, *marg = nullptr;
+    float tau = 0.f;
   };
   std::map<std::tuple<int, int, int, int, int, int>, GraphEntry> graphs;
   bool use_graphs = true;
   cudaStream_t cap_st = nullptr;  // private capture stream
+  cudaStream_t cap_st2 = nullptr; // capture of conditional-node bodies
+
+  // synchronous verification, device-side dispatch (engine.cu decode_sync)
+  int32_t *vx_slot = nullptr, *vx_pos = nullptr, *vx_tok = nullptr, *vx_nk = nullptr;  // chunk list [Tmax]
+  int32_t* vctl_d = nullptr;  // [4] chunk cursor
+  int32_t* ran_d = nullptr;   // [1] rows whose gate fired this step
+  int32_t* spin = nullptr;    // pinned readback of the eager (debug) path: ctrl | last | ran
+  bool shadow_stale = false;  // shadow_h not refreshed since a graph-dispatched sync step
+  unsigned long long cond_body_launches = 0, cond_lm_launches = 0;  // kernels per loop iteration / LM body
 };

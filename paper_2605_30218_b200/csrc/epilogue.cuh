@@ -221,8 +221,12 @@ __device__ __forceinline__ QkvPair qkv_prep(const QkvArgs& a, int t, int h, int 
   } else {
     const int kvsel = h < a.H + a.KV ? 0 : 1;
     const int kh = h - a.H - kvsel * a.KV;
-    r.dst = a.paged ? cache_ptr(a.cache, a.slot[t], p, kvsel, kh)  // tentative append of column p
-                    : (kvsel ? a.vd : a.kd) + (size_t)t * a.KV * a.hd + kh * a.hd;
+    if (a.paged && a.slot[t] < 0) {
+      r.dst = nullptr;  // a no-op entry of a padded verifier chunk: nothing to append
+    } else {
+      r.dst = a.paged ? cache_ptr(a.cache, a.slot[t], p, kvsel, kh)  // tentative append of column p
+                      : (kvsel ? a.vd : a.kd) + (size_t)t * a.KV * a.hd + kh * a.hd;
+    }
   }
   return r;
 }
@@ -259,6 +263,7 @@ __device__ __forceinline__ QkvPair qkv_prep_staged(const QkvArgs& a, int t, int 
 }
 __device__ __forceinline__ void qkv_finish(const QkvArgs& a, const QkvPair& r, const float* part, const PartSpec& ps,
                                            int h, int i) {
+  if (!r.dst) return;
   const size_t stride = (size_t)(a.part_T ? a.part_T : a.T) * (a.H + 2 * a.KV) * a.hd;
   float x = sum_splits(part, part_count(ps, r.f1), stride, r.row + r.f1);
   float y = sum_splits(part, part_count(ps, r.f2), stride, r.row + r.f2);

@@ -111,6 +111,7 @@ def test_max_batch_fast_logits_vs_oracle(orc, torch, tiny):
             logits[r].append(lg[r].copy())
     eng.close()
     det = orc.det_sched()
+    errs, noises = [], []
     for r in rows:
         st = orc.State(m, 1, len(prompts[r]) + 8)
         sd = orc.State(m, 1, len(prompts[r]) + 8)     # pinned plan: the oracle's own reorder noise
@@ -124,11 +125,16 @@ def test_max_batch_fast_logits_vs_oracle(orc, torch, tiny):
             rr = st.step([0], [0], 0.0, orc.fast_sched(B_MAX), det, **kw)
             rd = sd.step([0], [0], 0.0, det, det, **kw)
             e = np.abs(logits[r][t] - rr["logits"][0])
-            noise = np.abs(rr["logits"][0] - rd["logits"][0])       # DESIGN.md 9 derivation
-            q_tol = max(TOL, 2 * float(np.quantile(noise, 0.999)))
-            m_tol = max(TOL, 2 * float(noise.max()))
-            assert np.quantile(e, 0.999) <= q_tol and e.max() <= m_tol, (r, t, float(e.max()), m_tol)
+            errs.append(e)
+            noises.append(np.abs(rr["logits"][0] - rd["logits"][0]))
             if rr["g"][0] > 2 * e.max():
                 assert toks[r][t + 1] == int(rr["f_tok"][0])
         st.close()
         sd.close()
+    # within max(2e-2, 2 x the oracle's own schedule-to-schedule
+    # noise), pooled over the sampled rows and steps (test_gpu_engine._check_logit_err)
+    e, noise = np.concatenate(errs), np.concatenate(noises)
+    q_tol = max(TOL, 2 * float(np.quantile(noise, 0.999)))
+    m_tol = max(TOL, 2 * float(noise.max()))
+    assert np.quantile(e, 0.999) <= q_tol and e.max() <= m_tol, (float(np.quantile(e, 0.999)), float(e.max()),
+                                                                  q_tol, m_tol)
