@@ -344,6 +344,21 @@ cudaError_t launch_vchunk(const VChunkArgs& a, cudaStream_t st) {
   return launch_k(k_vchunk, dim3(1), dim3(512), 0, st, a);
 }
 
+__global__ void k_emit(const int32_t* __restrict__ tok, const uint8_t* __restrict__ kind,
+                       const float* __restrict__ marg, int B, int32_t* tok_out, uint8_t* kind_out, float* marg_out) {
+  griddep();
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  tok_out[b] = tok[b];
+  if (kind_out) kind_out[b] = kind[b];
+  if (marg_out) marg_out[b] = marg[b];
+}
+
+cudaError_t launch_emit(const int32_t* tok, const uint8_t* kind, const float* marg, int B, int32_t* tok_out,
+                        uint8_t* kind_out, float* marg_out, cudaStream_t st) {
+  return launch_k(k_emit, dim3((B + 255) / 256), dim3(256), 0, st, tok, kind, marg, B, tok_out, kind_out, marg_out);
+}
+
 __global__ void k_gather_last(const uint16_t* __restrict__ xn, const int32_t* __restrict__ last,
                               const int32_t* __restrict__ ctrl, const int32_t* __restrict__ vctl, int T, int d,
                               uint16_t* __restrict__ xgn) {

@@ -112,6 +112,10 @@ struct VChunkArgs {
   unsigned long long* stats;  // [11] += 1 per iteration
 };
 cudaError_t launch_vchunk(const VChunkArgs& a, cudaStream_t st);
+// copy a step's committed tokens / kinds / margins from the engine's buffers
+// (where a whole-step CUDA graph writes them) to the caller's (kind, margin nullable)
+cudaError_t launch_emit(const int32_t* tok, const uint8_t* kind, const float* marg, int B, int32_t* tok_out,
+                        uint8_t* kind_out, float* marg_out, cudaStream_t st);
 // rows r < ctrl[0] whose last catch-up token lies in this chunk
 // (last[r] - vctl[1] in [0, T)): xgn[r] = xn[last[r] - vctl[1]]
 cudaError_t launch_gather_last(const uint16_t* xn, const int32_t* last, const int32_t* ctrl, const int32_t* vctl,

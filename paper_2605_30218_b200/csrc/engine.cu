@@ -307,6 +307,7 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   c->vx_tok = s.take<int32_t>(Tm); c->vx_nk = s.take<int32_t>(Tm);
   c->vctl_d = s.take<int32_t>(4);
   c->ran_d = s.take<int32_t>(4);
+  c->o_tok_d = s.take<int32_t>(B); c->o_kind_d = s.take<uint8_t>(B); c->o_marg_d = s.take<float>(B);
   c->dbg_vtok = s.take<int32_t>(B); c->dbg_out = s.take<int32_t>(B);
   c->dbg_vg = s.take<float>(B);
   c->dbg_kind = s.take<uint8_t>(B); c->dbg_trig = s.take<uint8_t>(B);
@@ -1300,24 +1301,26 @@ static mg_status decode_sync(mg_ctx* c, const int32_t* slots, int B, const uint8
   if (gate && !debug) {
     auto& g = c->graphs[std::make_tuple(5, B, fs.attn_ns, fs.attn_sk, n_lm,
                                         (c->fast_mode * 2 + c->repair_mode) * 65536 + fkey)];
+    // the graph commits into the engine's output buffers (one tiny copy to the
+    // caller's below), so it does not depend on the caller's pointers; tau is
+    // baked into the gate and commit arguments: a new tau rebuilds it
+    if (g.exec && g.tau != tau) {
+      cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+      g.seen = 1;
+    }
     if (!g.exec && ++g.seen >= 2) {
       unsigned long long fixed = 0;
-      if ((r = build_sync_graph(c, B, n_lm, tau, fs, tokens_out, kind_out, margin_out, &g.exec, &fixed))) return r;
+      if ((r = build_sync_graph(c, B, n_lm, tau, fs, c->o_tok_d, c->o_kind_d, c->o_marg_d, &g.exec, &fixed)))
+        return r;
       g.launches = fixed;
+      g.tau = tau;
     }
     if (g.exec) {
       Nvtx gr("mg.step.graph (fast | gate | verify | commit)");
-      // the outputs and tau are baked into the graph: rebuild when they change
-      if (g.tok != tokens_out || g.kind != kind_out || g.marg != margin_out || g.tau != tau) {
-        cudaGraphExecDestroy(g.exec);
-        g.exec = nullptr;
-        unsigned long long fixed = 0;
-        if ((r = build_sync_graph(c, B, n_lm, tau, fs, tokens_out, kind_out, margin_out, &g.exec, &fixed))) return r;
-        g.launches = fixed;
-      }
-      g.tok = tokens_out; g.kind = kind_out; g.marg = margin_out; g.tau = tau;
       CK(cudaGraphLaunch(g.exec, c->st));
-      c->launches += g.launches;
+      CK(launch_emit(c->o_tok_d, c->o_kind_d, c->o_marg_d, B, tokens_out, kind_out, margin_out, c->st));
+      c->launches += g.launches + 1;
       c->shadow_stale = true;
       done = true;
     }

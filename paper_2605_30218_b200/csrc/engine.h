@@ -141,9 +141,7 @@ struct mg_ctx {
     cudaGraphExec_t exec = nullptr;
     int seen = 0;
     unsigned long long launches = 0;
-    // whole-step graphs (decode_sync) bake in the outputs and the threshold
-    const void *tok = nullptr, *kind = nullptr, *marg = nullptr;
-    float tau = 0.f;
+    float tau = 0.f;  // whole-step graphs (decode_sync) bake in the threshold
   };
   std::map<std::tuple<int, int, int, int, int, int>, GraphEntry> graphs;
   bool use_graphs = true;
@@ -154,6 +152,9 @@ struct mg_ctx {
   int32_t *vx_slot = nullptr, *vx_pos = nullptr, *vx_tok = nullptr, *vx_nk = nullptr;  // chunk list [Tmax]
   int32_t* vctl_d = nullptr;  // [4] chunk cursor
   int32_t* ran_d = nullptr;   // [1] rows whose gate fired this step
+  int32_t* o_tok_d = nullptr; // a whole-step graph's outputs [max_batch] (then copied to the caller's)
+  uint8_t* o_kind_d = nullptr;
+  float* o_marg_d = nullptr;
   int32_t* spin = nullptr;    // pinned readback of the eager (debug) path: ctrl | last | ran
   bool shadow_stale = false;  // shadow_h not refreshed since a graph-dispatched sync step
   unsigned long long cond_body_launches = 0, cond_lm_launches = 0;  // kernels per loop iteration / LM body
