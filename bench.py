@@ -189,7 +189,7 @@ def run_gpu(args):
     keys = ["steps", "rows", "protected_rows", "triggers", "verified", "repairs", "verifier_launches",
             "catchup_tokens"]
 
-    def run_arm(tau, prot, timing=False, clocks=None, pipelined=False, fused=False):
+    def run_arm(tau, prot, timing=False, clocks=None, pipelined=False, fused=False, arm_prompts=None):
         """Fresh deterministic prefill, W warm-up steps, K timed steps (CUDA events
         on the engine's stream, barrier + synchronize on both sides).
         pipelined: MG_VERIFY_PIPELINED (include/mg.h) -- a gated row's
@@ -200,7 +200,8 @@ def run_gpu(args):
             except Exception:
                 pass
         eng.set_policy(verify_mode=1 if pipelined else (2 if fused else 0))
-        first = [eng.prefill(i, p) for i, p in enumerate(prompts)]
+        ps = arm_prompts or prompts
+        first = [eng.prefill(i, p) for i, p in enumerate(ps)]
         s0 = eng.stats()
         toks, kinds_w = [], []
         for _ in range(W):
@@ -250,7 +251,7 @@ def run_gpu(args):
         if pipelined:  # resolve the last tentative tokens (untimed)
             pos, last, _ = eng.verify_window(list(range(B)))
             for b in range(B):
-                n = int(pos[b]) - len(prompts[b]) + 1
+                n = int(pos[b]) - len(ps[b]) + 1
                 del seqs[b][n:]
                 seqs[b][-1] = int(last[b])
             eng.set_policy(verify_mode=0)
@@ -273,6 +274,10 @@ def run_gpu(args):
         t100 = calib["tau100"] if calib["tau100"] is not None else math.inf
         _, (tau,) = sharding.aggregate([], [t100], device="cuda")
     res = {"bf16": run_arm(0.0, None)}
+    # the round-1 reference point: the BF16 step at the mid-decode context (~400)
+    ctx_mid = prompt_len + decode_len // 2 - W
+    res["bf16_mid"] = run_arm(0.0, None, arm_prompts=inputs.prompts(B, ctx_mid, shp["vocab"],
+                                                                     seed=7 + sharding.rank_requests(rank, ws, B)[0]))
     res["mg"] = run_arm(tau, head, clocks=Clocks(local))
     res["ao"] = run_arm(math.inf, head)
     # pipelined verification (include/mg.h MG_VERIFY_PIPELINED): always-on with the
@@ -379,8 +384,8 @@ def run_gpu(args):
     def det(a, b, prot):
         return sum(1 for i in range(B) if prot[i] and res[a]["seqs"][i] == res[b]["seqs"][i]), int(prot.sum())
 
-    arms = [a for a in ("bf16", "mg", "ao", "ao_pipe", "mg_fused", "ao_fused", "mg_other", "ao_other", "ao_pipe_other",
-                        "ao_fused_other") if a in res]
+    arms = [a for a in ("bf16", "bf16_mid", "mg", "ao", "ao_pipe", "mg_fused", "ao_fused", "mg_other", "ao_other",
+                        "ao_pipe_other", "ao_fused_other") if a in res]
 
     def det_prefix(a, b, prot):  # pipelined rows may be shorter (a repair costs a step): common prefix
         ok = 0
@@ -442,7 +447,9 @@ def run_gpu(args):
                 "note": "MG_VERIFY_PIPELINED: the verifier of step t rides on step t+1's weight pass "
                         "(tokens = emitted - replaced); determinism = common prefix equal to the sync always-on run"}
 
-    arms_out = {"bf16_tok_s": round(tok / (T["bf16"] * 1e-3), 2), "tau": tau,
+    arms_out = {"bf16_tok_s": round(tok / (T["bf16"] * 1e-3), 2),
+                "bf16_mid_decode_tok_s": round(tok / (T["bf16_mid"] * 1e-3), 2),
+                "bf16_mid_decode_ctx": f"{ctx_mid + W}..{ctx_mid + W + K}", "tau": tau,
                 "tau_source": "calibrated tau100 (seeds 10^6 + i)" if calib else "--tau",
                 "headline": summary("mg", "ao", dh, args.protected)}
     if calib:
@@ -515,6 +522,7 @@ def run_gpu(args):
                      # the whole pipelined BF16 step (CUDA graph, PDL) against the same peak:
                      # algorithmic bytes = weights once + every row's K/V context
                      "step": _step_roofline(shp, B, ctx0 + W + K // 2, T["bf16"] / K, hbm),
+                     "step_mid_decode": _step_roofline(shp, B, ctx_mid + W + K // 2, T["bf16_mid"] / K, hbm),
                      # the synchronous verifier launches against the same peak --
                      # time = always-on step - BF16 step; bytes = weights once + the verified
                      # rows' shadow K/V (one protected row / all rows)
@@ -1055,16 +1063,20 @@ def run_full_decode(args, pnames=("one", "all"), eng=None):
         prot = inputs.protected_mask(B, pname)
         r = {n: _decode_run(eng, ev, t, prot, W, K, timed=True, fused=f)
              for n, t, f in (("bf16", 0.0, False), ("margingate", t100, False), ("always_on", math.inf, False),
-                             ("margingate_fused", t100, True), ("always_on_fused", math.inf, True))}
+                             ("margingate_fused", t100, True), ("always_on_fused", math.inf, True),
+                             # the argmax-bound threshold 2 max eps: covers every flip
+                             # the calibration saw, at a higher trigger rate than tau100
+                             ("margingate_tau_p", cal["tau_p"], False))}
         pr = [i for i in range(B) if prot[i]]
         ref = r["always_on"][0]
         out[pname] = {
             "tok_s": {n: round(B * K / (v[2] * 1e-3), 2) for n, v in r.items()},
             "inc": {n: round(metrics.latency_increment(v[2], r["bf16"][2]), 4) for n, v in r.items() if n != "bf16"},
             "trigger_pct": round(100 * metrics.rates(r["margingate"][1])["r_verify"], 3),
+            "trigger_pct_tau_p": round(100 * metrics.rates(r["margingate_tau_p"][1])["r_verify"], 3),
             "determinism_pct": {n: round(100 * metrics.seq_determinism([r[n][0][i] for i in pr],
                                                                        [ref[i] for i in pr]), 2)
-                                for n in ("bf16", "margingate", "margingate_fused")}}
+                                for n in ("bf16", "margingate", "margingate_fused", "margingate_tau_p")}}
         inc_mg, inc_ao = out[pname]["inc"]["margingate"], out[pname]["inc"]["always_on"]
         out[pname]["increment_ratio"] = round(metrics.increment_ratio(inc_ao, inc_mg), 3) if inc_mg > 0.01 else None
     if own:

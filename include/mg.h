@@ -82,7 +82,13 @@ typedef struct {
 
 /* Device-side counters, summed over all steps since mg_init.
  * r_verify = triggers / protected_rows, r_repair = repairs / protected_rows
- * (PAPER.md:215). */
+ * (PAPER.md:215).  protected_rows counts the gate decisions of protected rows
+ * (in MG_VERIFY_PIPELINED a kind-4 replacement step makes none: its fast
+ * output is dropped), so r_verify = 1 at tau = +inf in every verify mode.
+ * verifier_launches / catchup_tokens count the verifier's work: in
+ * MG_VERIFY_SYNC every protected row is caught up when the verifier runs, in
+ * MG_VERIFY_FUSED on every step (speculative); tentative tokens resolved by
+ * mg_verify_window count as window_rows, not as verified / repairs. */
 typedef struct {
   uint64_t steps, rows, protected_rows, triggers, verified, repairs, verifier_launches, catchup_tokens;
   /* windowed verification (mg_verify_window): rows verified, rows rolled
