@@ -38,9 +38,6 @@
 namespace mg {
 
 constexpr int kAtThreads = 128;
-#ifndef MG_ATTN_EPI_IT
-#define MG_ATTN_EPI_IT 3
-#endif
 
 // Per warp: a ring of RK K blocks and a separate ring of RV V blocks, each
 // with its own mbarriers, so the K block of step i + RK is requested as soon as
@@ -200,36 +197,14 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
     const size_t stride = (size_t)(a.part_T ? a.part_T : a.T) * NQKV, row = (size_t)t * NQKV;
     const int p = a.pos[t];
     const int nq = G * h2, nitems = nq + (has_new ? 2 * h2 : 0);
-    // MG_ATTN_EPI_IT items per thread per round: every partial load of a
-    // round's items is issued before any of them is used (one L2 round trip
-    // per round instead of one per item); sums and rounding unchanged
-    constexpr int IT = MG_ATTN_EPI_IT;
-    for (int w0 = threadIdx.x; w0 < nitems; w0 += IT * kAtThreads) {
-    float xs[IT], ys[IT];
-#pragma unroll
-    for (int k = 0; k < IT; ++k) {
-      const int w = w0 + k * kAtThreads;
-      xs[k] = ys[k] = 0.f;
-      if (w < nitems) {
-        const bool isq = w < nq;
-        const int g = isq ? w / h2 : (w - nq) / h2;
-        const int i = (isq ? w : w - nq) % h2;
-        const int h = isq ? kvh * G + g : H + g * a.KV + kvh;
-        const int f1 = h * HD + i, f2 = f1 + h2;
-        xs[k] = sum_splits(a.qkv_part, part_count(a.qkv_ps, f1), stride, row + f1);
-        ys[k] = sum_splits(a.qkv_part, part_count(a.qkv_ps, f2), stride, row + f2);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < IT; ++k) {
-      const int w = w0 + k * kAtThreads;
-      if (w >= nitems) continue;
+    for (int w = threadIdx.x; w < nitems; w += kAtThreads) {
       const bool isq = w < nq;
       const int g = isq ? w / h2 : (w - nq) / h2;  // q: head in group; k/v: 0 = K, 1 = V
       const int i = (isq ? w : w - nq) % h2;
       const int h = isq ? kvh * G + g : H + g * a.KV + kvh;
       const int f1 = h * HD + i, f2 = f1 + h2;
-      float x = xs[k], y = ys[k];
+      float x = sum_splits(a.qkv_part, part_count(a.qkv_ps, f1), stride, row + f1);
+      float y = sum_splits(a.qkv_part, part_count(a.qkv_ps, f2), stride, row + f2);
       if (a.bias) {
         x = __fadd_rn(x, bf2f(a.bias[f1]));
         y = __fadd_rn(y, bf2f(a.bias[f2]));
@@ -254,7 +229,6 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
         dst[i] = oa;
         dst[i + h2] = ob;
       }
-    }
     }
     __syncthreads();
   }

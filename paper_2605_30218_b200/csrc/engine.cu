@@ -1448,6 +1448,10 @@ mg_status mg_init(const mg_config* cfg, const mg_buffers* bufs, void* stream, mg
   cudaEventRecord(c->stage_ev[0], c->st);
   cudaEventRecord(c->stage_ev[1], c->st);
   {
+    // MG_NO_GRAPHS=1: every step eager (sanitizers and ncu kernel-level
+    // profiling, which do not follow kernels inside conditional graph nodes)
+    const char* ng = getenv("MG_NO_GRAPHS");
+    c->use_graphs = !(ng && ng[0] == '1');
     const char* lu = getenv("MG_LM_UNFUSED");  // A/B knob: logits + separate top-2 kernels
     c->lm_unfused = lu && lu[0] == '1';
     const char* fs = getenv("MG_FAST_SK");  // measurement knobs: attention split sizes
