@@ -11,7 +11,7 @@ on the GPU's committed tokens:
 * fast logits of the sampled row against the oracle's (batch-shaped
   schedule), and verifier (tau = inf) logits against the oracle's
   deterministic forward, within max(north-star 2e-2, 2x the oracle's own
-  schedule-to-schedule discrepancy at this depth) -- at 28-48 layers two
+  schedule-to-schedule discrepancy at this depth, pooled over the steps) -- at 28-48 layers two
   valid fp32 summation orders already differ by ~0.03-0.04 (p99.9) because
   bf16 activation roundings flip and propagate; the argmax is
   checked exactly wherever the margin exceeds 2x the observed error
@@ -107,13 +107,18 @@ def test_full_size_sampled_row_parity(orc, name):
     D = orc.State(m, 1, plen + steps + 2)
     if A.prefill(0, prompts[row], det) != toks[0] or D.prefill(0, prompts[row], det) != toks[0]:
         pytest.skip("first token inside the argmax-ambiguity band")
+    ras, rds = [], []
     for t in range(steps):
         kw = dict(forced_trig=[1], forced_out=[toks[t + 1]], forced_kind=[1], want_logits=True)
-        ra = A.step([0], [1], INF, orc.fast_sched(B), det, **kw)
-        rd = D.step([0], [1], INF, det, det, **kw)
-        noise = np.abs(ra["logits"][0] - rd["logits"][0])
-        q_tol = max(TOL, 2 * float(np.quantile(noise, 0.999)))
-        m_tol = max(1.5 * TOL, 2 * float(noise.max()))
+        ras.append(A.step([0], [1], INF, orc.fast_sched(B), det, **kw))
+        rds.append(D.step([0], [1], INF, det, det, **kw))
+    # the oracle's own schedule-to-schedule spread, pooled over the
+    # steps (one step's spread is a single sample of the flip tail)
+    noise = np.concatenate([np.abs(ra["logits"][0] - rd["logits"][0]) for ra, rd in zip(ras, rds)])
+    q_tol = max(TOL, 2 * float(np.quantile(noise, 0.999)))
+    m_tol = max(TOL, 2 * float(noise.max()))
+    for t in range(steps):
+        ra, rd = ras[t], rds[t]
         ef = np.abs(fl[t] - ra["logits"][0])
         print(f"[fullsize] {name} step {t}: gpu-vs-oracle p99.9 {np.quantile(ef, 0.999):.4f} max {ef.max():.4f}; "
               f"oracle self-noise p99.9 {np.quantile(noise, 0.999):.4f} max {noise.max():.4f}")

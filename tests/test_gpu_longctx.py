@@ -161,3 +161,58 @@ def test_long_context_parity(orc, name):
     m.close()
     print(f"[longctx] {name}: checked {checked}")
     assert checked["fast_tok"] >= len(rows) and checked["ver_rows"] >= len(rows)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_long_context_verify_modes_agree(mode):
+    """Past 512 keys at batch 64 (the fast plan and the verifier's pinned plan
+    differ), the pipelined (1) and fused (2) verify modes commit exactly the
+    synchronous mode's tokens and repairs (include/mg.h), at a finite tau with
+    real triggers and repairs and every row protected (the 8B attention shape,
+    prompts 520-700)."""
+    import torch
+
+    from paper_2605_30218_b200.engine import Engine
+    shp = inputs.shape("longattn")
+    B, steps = 64, 10
+    lengths = inputs.ragged_lengths(B, 520, 700, seed=98)
+    prompts = inputs.prompts(B, lengths, shp["vocab"], seed=5100)
+    runs = {}
+    for m in (0, mode):
+        eng = Engine(shp, max_batch=B, max_slots=B, max_seq=max(lengths) + steps + 4, page_size=64)
+        eng.set_policy(verify_mode=m)
+        seqs = [[eng.prefill(i, p)] for i, p in enumerate(prompts)]
+        out = torch.empty(B, dtype=torch.int32, device="cuda")
+        kind = torch.empty(B, dtype=torch.uint8, device="cuda")
+        tau = None
+        for t in range(steps):
+            if tau is None:                  # the median margin of the first step: real decisions both ways
+                eng.step(list(range(B)), None, INF, out, kind)
+                tau = _finite_tau(eng.last_step(B)["g"])
+            else:
+                eng.step(list(range(B)), None, tau, out, kind)
+            o, k = out.cpu().numpy(), kind.cpu().numpy()
+            for b in range(B):
+                if m == 1 and k[b] == 4:
+                    seqs[b][-1] = int(o[b])
+                else:
+                    seqs[b].append(int(o[b]))
+        if m == 1:
+            pos, last, _ = eng.verify_window(list(range(B)))
+            for b in range(B):
+                n = int(pos[b]) - len(prompts[b]) + 1
+                del seqs[b][n:]
+                seqs[b][-1] = int(last[b])
+        st = eng.stats()
+        eng.close()
+        runs[m] = (seqs, st)
+    ref, st0 = runs[0]
+    got, st1 = runs[mode]
+    if mode == 2:
+        assert got == ref
+        assert (st1["triggers"], st1["verified"], st1["repairs"]) == (st0["triggers"], st0["verified"], st0["repairs"])
+    else:
+        for b in range(B):
+            n = min(len(got[b]), len(ref[b]))
+            assert n >= steps - 2 and got[b][:n] == ref[b][:n], b
+    assert st0["triggers"] > 0
