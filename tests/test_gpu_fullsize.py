@@ -46,11 +46,12 @@ def _host_ram_ok(shp):
     return psutil.virtual_memory().available > 2.5 * 2 * n
 
 
-def _bench_max_seq():
-    """bench.py's context capacity for the MATH500 workload (W=8, K=32)."""
+def _bench_max_seq(W=5, K=20):
+    """bench.py's context capacity for the MATH500 workload: the timed steps
+    end the decode (ctx0 = prompt + decode - W - K), at the driver's W / K."""
     p, d = inputs.WORKLOADS["math500"]
-    ctx0 = p + d // 2 - 8
-    return ctx0 + 8 + 32 + 2
+    ctx0 = max(p, p + d - W - K)
+    return ctx0 + W + K + 2
 
 
 @pytest.mark.parametrize("name", list(CASES))

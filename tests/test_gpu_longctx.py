@@ -45,8 +45,8 @@ INF = float("inf")
 #          0 = shortest; -1 = longest)
 CASES = {
     "wide": (64, (520, 1100), (0,)),
-    "longattn": (64, (520, 1100), (0, 32, -1)),
-    "dsr1attn": (64, (2000, 4000), (20,)),
+    "longattn": (64, (520, 1100), (0, -1)),
+    "dsr1attn": (64, (2000, 4000), (8,)),
 }
 
 
