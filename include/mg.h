@@ -26,11 +26,11 @@
  *    set by the gate kernel.  Exceptions, all debug or first-use: the first
  *    step of a new (batch, protected-count) shape and steps with logit
  *    captures / timing / injected noise (include/mg_debug.h) run the same
- *    kernels eagerly and read the gate back once.  The threshold is baked
- *    into the step graph: a step with a different tau than the previous one
- *    of the same shape rebuilds it (a per-step varying tau pays a graph
- *    instantiation per step).  Device outputs are valid after stream
- *    completion.  mg_stats, mg_prefill and mg_verify_window synchronise.
+ *    kernels eagerly and read the gate back once.  The slots, the mask and
+ *    the threshold travel in the step's single H2D copy and the graph reads
+ *    them from device memory, so a per-step threshold costs nothing extra.
+ *    Device outputs are valid after stream completion.  mg_stats,
+ *    mg_prefill and mg_verify_window synchronise.
  *  - Host arrays: the slots and the protection mask of a step are HOST
  *    arrays (SURVEY 8(b) lists device pointers): the host owns the page
  *    allocator and the capacity checks (MG_ERR_CAPACITY before any state

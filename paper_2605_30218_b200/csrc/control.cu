@@ -140,10 +140,10 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
       tr = a.prot ? a.prot[b] != 0 : true;
     } else if (a.eager) {  // synchronous: list every protected row, count the rows whose gate fires
       tr = a.prot ? a.prot[b] != 0 : true;
-      if (tr && gate_fires(a.g[b], a.tau)) atomicAdd(&s_fired, 1);  // strict <
+      if (tr && gate_fires(a.g[b], a.tau_d ? *a.tau_d : a.tau)) atomicAdd(&s_fired, 1);  // strict <
     } else {
       const bool prot = a.prot ? a.prot[b] != 0 : true;
-      tr = prot && gate_fires(a.g[b], a.tau);  // strict <
+      tr = prot && gate_fires(a.g[b], a.tau_d ? *a.tau_d : a.tau);  // strict <
     }
   }
   const int gap = tr ? (p - s0 + 1) : 0;
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(256) k_commit(CommitArgs a) {
   const int slot = a.slots[b];
   const int p = a.pos[slot];
   const bool listed = a.gate_ran && a.trig[b] && (!a.ran || a.ran[0] > 0);
-  const bool tr = listed && (!a.spec || gate_fires(a.g[b], a.spec_tau));  // fused mode: the gate
+  const bool tr = listed && (!a.spec || gate_fires(a.g[b], a.tau_d ? *a.tau_d : a.spec_tau));  // the gate
   const int f = a.f_tok[b];
   const int v = tr ? a.v_tok[a.rank[b]] : -1;
   const int kind = !tr ? 0 : (v == f ? 1 : 2);

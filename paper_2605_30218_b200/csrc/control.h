@@ -46,6 +46,7 @@ struct GateArgs {
   unsigned long long h_loop, h_lm;
   int32_t* vctl;
   unsigned long long* stats;  // [12] += 1 when the LM-head IF body runs (launch accounting)
+  const float* tau_d;         // nullable: the step's threshold in device memory (overrides tau)
 };
 cudaError_t launch_gate(const GateArgs& a, cudaStream_t st);
 
@@ -83,6 +84,7 @@ struct CommitArgs {
   // MG_VERIFY_SYNC (eager catch-up): the listed rows were verified only if
   // ran[0] > 0 (nullable: always)
   const int32_t* ran;
+  const float* tau_d;      // nullable: spec_tau in device memory (overrides spec_tau)
   int32_t* tokens_out;
   uint8_t* kind_out;
   float* margin_out;

@@ -278,8 +278,12 @@ static void carve(mg_ctx* c, void* wbase, void* kvf, void* kvs, void* ws, Layout
   c->pt_d = s.take<int32_t>((size_t)g.max_slots * c->max_pages);
   c->stats_d = s.take<unsigned long long>(16);
   c->nan_d = s.take<int32_t>(4);
-  c->slots_d = s.take<int32_t>(B);
-  c->prot_d = s.take<uint8_t>(B);
+  c->batch_pw = (B + 3) / 4;
+  c->batch_d = s.take<int32_t>((size_t)B + c->batch_pw + 4 + 2 * (size_t)B);
+  c->slots_d = c->batch_d;
+  c->prot_d = c->batch_d ? reinterpret_cast<uint8_t*>(c->batch_d + B) : nullptr;
+  c->tau_d = c->batch_d ? reinterpret_cast<float*>(c->batch_d + B + c->batch_pw) : nullptr;
+  c->ptu_d = c->batch_d ? c->batch_d + B + c->batch_pw + 4 : nullptr;
   c->f_slot = s.take<int32_t>(B); c->f_pos = s.take<int32_t>(B); c->f_tok = s.take<int32_t>(B);
   c->f_nk = s.take<int32_t>(B); c->f_i2 = s.take<int32_t>(B);
   c->f_g = s.take<float>(B); c->f_v1 = s.take<float>(B); c->f_v2 = s.take<float>(B);
@@ -569,31 +573,37 @@ static mg_status apply_pt(mg_ctx* c, const std::vector<std::pair<int, int>>& upd
   return MG_OK;
 }
 
-// One H2D copy per step: the batch's slots, its protection bytes (packed) and
-// the page-table entries of the pages its rows now enter; then slots_d /
-// prot_d and the page table on the device.
-static mg_status upload_batch(mg_ctx* c, const int32_t* slots, int B, const uint8_t* prot) {
+// One H2D copy per step, straight into the engine's batch block (batch_d):
+// the batch's slots, its protection bytes (packed), the threshold and the
+// page-table entries of the pages its rows now enter (applied by k_apply_pt).
+// slots_d / prot_d / tau_d are fixed addresses inside the block, so the step
+// graphs read each step's values without copies on the device.
+static mg_status upload_batch(mg_ctx* c, const int32_t* slots, int B, const uint8_t* prot, float tau) {
   std::vector<std::pair<int, int>> upd;
   for (int b = 0; b < B; ++b) {
     const int s = slots[b];
     if (c->pos_h[s] / c->PS >= (int)c->pages[s].size()) alloc_page(c, s, &upd);
   }
-  const int pw = (B + 3) / 4;  // prot bytes packed in words
-  std::vector<int32_t> w(B + pw + 2 * upd.size());
-  memcpy(w.data(), slots, B * 4);
-  std::vector<uint8_t> pb(pw * 4, 1);
-  if (prot) memcpy(pb.data(), prot, B);
-  memcpy(w.data() + B, pb.data(), pw * 4);
-  for (size_t i = 0; i < upd.size(); ++i) {
-    w[B + pw + 2 * i] = upd[i].first;
-    w[B + pw + 2 * i + 1] = upd[i].second;
+  const int MB = c->cfg.max_batch, pw = c->batch_pw;
+  const size_t words = (size_t)MB + pw + 4 + 2 * upd.size();
+  if (words > c->stage_words) return fail(c, MG_ERR_INVALID, "staging overflow");
+  const int i = c->stage_idx;
+  c->stage_idx ^= 1;
+  CK(cudaEventSynchronize(c->stage_ev[i]));
+  int32_t* h = c->pinned + i * c->stage_words;
+  memcpy(h, slots, (size_t)B * 4);
+  uint8_t* pb = reinterpret_cast<uint8_t*>(h + MB);
+  memset(pb, 1, (size_t)pw * 4);
+  if (prot) memcpy(pb, prot, B);
+  memcpy(h + MB + pw, &tau, 4);
+  for (size_t k = 0; k < upd.size(); ++k) {
+    h[MB + pw + 4 + 2 * k] = upd[k].first;
+    h[MB + pw + 4 + 2 * k + 1] = upd[k].second;
   }
-  mg_status r = upload(c, w);
-  if (r) return r;
-  CK(cudaMemcpyAsync(c->slots_d, c->staging_d, B * 4, cudaMemcpyDeviceToDevice, c->st));
-  CK(cudaMemcpyAsync(c->prot_d, c->staging_d + B, B, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(c->batch_d, h, words * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaEventRecord(c->stage_ev[i], c->st));
   if (!upd.empty()) {
-    k_apply_pt<<<cdiv((int)upd.size(), 128), 128, 0, c->st>>>(c->pt_d, c->staging_d + B + pw, (int)upd.size());
+    k_apply_pt<<<cdiv((int)upd.size(), 128), 128, 0, c->st>>>(c->pt_d, c->ptu_d, (int)upd.size());
     CK(cudaGetLastError());
     c->launches++;
   }
@@ -789,7 +799,7 @@ static mg_status decode_pipelined(mg_ctx* c, const int32_t* slots, int B, const 
   for (int s = 0; s < S; ++s) n_pend += c->active[s] && c->pend_h[s];
   size_t ev0 = 0;
   if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
-  if ((r = upload_batch(c, slots, B, prot))) return r;
+  if ((r = upload_batch(c, slots, B, prot, tau))) return r;
   // the pending list built at the end of the previous step (device ctrl / last / cu_*);
   // rebuilt here (pending-list gate over this batch) when mg_verify_window or
   // mg_release changed the pending set since
@@ -963,7 +973,7 @@ static mg_status decode_fused(mg_ctx* c, const int32_t* slots, int B, const uint
   const int n_list = (int)last.size();
   size_t ev0 = 0;
   if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
-  mg_status r = upload_batch(c, slots, B, prot);
+  mg_status r = upload_batch(c, slots, B, prot, tau);
   if (r) return r;
   GateArgs ga{};
   ga.g = c->f_g; ga.prot = c->prot_d; ga.tau = tau; ga.slots = c->slots_d; ga.B = B;
@@ -1096,6 +1106,7 @@ static GateArgs sync_gate_args(mg_ctx* c, int B, float tau) {
   ga.trig = c->trig_d; ga.rank = c->rank_d; ga.ctrl = c->ctrl_d; ga.last = c->last_d;
   ga.cu_slot = c->cu_slot; ga.cu_pos = c->cu_pos; ga.cu_tok = c->cu_tok; ga.cu_nk = c->cu_nk;
   ga.eager = 1; ga.ran = c->ran_d; ga.vctl = c->vctl_d;
+  ga.tau_d = c->tau_d;  // this step's threshold (upload_batch): the step graph does not depend on it
   return ga;
 }
 
@@ -1108,6 +1119,7 @@ static CommitArgs sync_commit_args(mg_ctx* c, int B, float tau, bool gate, int32
   ca.copy = col_copy(c, true);
   ca.repair_copy = c->repair_mode == MG_REPAIR_COLUMN ? 1 : 0;
   ca.spec = 1; ca.spec_tau = tau;  // listed = protected; the gate picks the committed verifier tokens
+  ca.tau_d = c->tau_d;
   ca.ran = gate ? c->ran_d : nullptr;
   ca.tokens_out = tokens_out; ca.kind_out = kind_out; ca.margin_out = margin_out; ca.stats = c->stats_d;
   ca.dbg_vtok = c->dbg_vtok; ca.dbg_vg = c->dbg_vg; ca.dbg_kind = c->dbg_kind; ca.dbg_trig = c->dbg_trig;
@@ -1288,7 +1300,7 @@ static mg_status decode_sync(mg_ctx* c, const int32_t* slots, int B, const uint8
   if ((int)c->free_pages.size() < need_pages) return fail(c, MG_ERR_CAPACITY, "KV pages exhausted");
   size_t ev0 = 0;
   if (c->timing.on) { ev0 = c->timing.used; cudaEventRecord(tevent(c), c->st); }
-  mg_status r = upload_batch(c, slots, B, prot);  // one H2D copy: slots, mask, page-table entries
+  mg_status r = upload_batch(c, slots, B, prot, tau);  // one H2D copy: slots, mask, page-table entries
   if (r) return r;
   const bool gate = n_prot > 0 && tau > 0.f;
   Sched fs = sched_fast(c, B, max_ctx);
@@ -1302,19 +1314,13 @@ static mg_status decode_sync(mg_ctx* c, const int32_t* slots, int B, const uint8
     auto& g = c->graphs[std::make_tuple(5, B, fs.attn_ns, fs.attn_sk, n_lm,
                                         (c->fast_mode * 2 + c->repair_mode) * 65536 + fkey)];
     // the graph commits into the engine's output buffers (one tiny copy to the
-    // caller's below), so it does not depend on the caller's pointers; tau is
-    // baked into the gate and commit arguments: a new tau rebuilds it
-    if (g.exec && g.tau != tau) {
-      cudaGraphExecDestroy(g.exec);
-      g.exec = nullptr;
-      g.seen = 1;
-    }
+    // caller's below) and reads tau from the uploaded batch block, so it
+    // depends on neither the caller's pointers nor the threshold
     if (!g.exec && ++g.seen >= 2) {
       unsigned long long fixed = 0;
       if ((r = build_sync_graph(c, B, n_lm, tau, fs, c->o_tok_d, c->o_kind_d, c->o_marg_d, &g.exec, &fixed)))
         return r;
       g.launches = fixed;
-      g.tau = tau;
     }
     if (g.exec) {
       Nvtx gr("mg.step.graph (fast | gate | verify | commit)");

@@ -105,6 +105,12 @@ struct mg_ctx {
   // batch / step buffers
   int32_t *slots_d, *f_slot, *f_pos, *f_tok, *f_nk, *f_i2;
   uint8_t* prot_d;
+  // a step's host inputs, one H2D copy into batch_d: [slots: max_batch][prot
+  // bytes: ceil(max_batch/4) words][tau][3 pad][page-table updates: 2 per row]
+  int32_t* batch_d = nullptr;
+  float* tau_d = nullptr;
+  int32_t* ptu_d = nullptr;
+  int batch_pw = 0;
   float *f_g, *f_v1, *f_v2;
   uint8_t* trig_d;
   int32_t *rank_d, *ctrl_d, *last_d;
@@ -141,7 +147,6 @@ struct mg_ctx {
     cudaGraphExec_t exec = nullptr;
     int seen = 0;
     unsigned long long launches = 0;
-    float tau = 0.f;  // whole-step graphs (decode_sync) bake in the threshold
   };
   std::map<std::tuple<int, int, int, int, int, int>, GraphEntry> graphs;
   bool use_graphs = true;

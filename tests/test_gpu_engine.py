@@ -401,12 +401,15 @@ def test_sync_graph_dispatch_equals_eager(torch, tiny):
     the chunk size, IF on the LM head; include/mg.h): the committed tokens,
     kinds and counters equal the eager form's (the debug path with one host
     readback of the gate), with real triggers, changing protection masks and
-    multi-token catch-ups (verify_chunk 16: several loop iterations)."""
+    multi-token catch-ups (verify_chunk 16: several loop iterations) and a
+    threshold that changes every step (uploaded with the batch, not baked
+    into the graph)."""
     shp, _ = tiny
-    B, steps, tau = 6, 30, 0.3
+    B, steps = 6, 30
     prompts = inputs.prompts(B, inputs.ragged_lengths(B, 8, 23, seed=93), shp["vocab"], seed=430)
     rng = np.random.default_rng(7)
     masks = [(rng.random(B) < (0.15 if t % 7 else 0.9)).astype(np.uint8) for t in range(steps)]
+    taus = [(0.3, 0.1, INF, 0.6)[t % 4] for t in range(steps)]   # a per-step threshold (read on the device)
     runs = []
     for eager in (True, False):
         eng = _engine(shp, B, verify_chunk=16)
@@ -418,7 +421,7 @@ def test_sync_graph_dispatch_equals_eager(torch, tiny):
         kind = torch.empty(B, dtype=torch.uint8, device="cuda")
         kinds = []
         for t in range(steps):
-            eng.step(list(range(B)), masks[t], tau, out, kind)
+            eng.step(list(range(B)), masks[t], taus[t], out, kind)
             o = out.cpu().numpy()
             kinds.append(kind.cpu().numpy().copy())
             for b in range(B):
