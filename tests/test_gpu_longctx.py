@@ -28,7 +28,7 @@ Cases: "wide" (Llama-3.1-8B widths, 2 layers, full 128256 vocabulary,
 prompts 520-1100); "longattn" (Llama-8B attention shape on a narrow model,
 prompts 520-1100, 2-3 pinned verifier splits); "dsr1attn"
 (DSR1-Distill-Qwen-7B attention shape -- 4 KV heads, qkv bias -- on a
-narrow model, prompts 2000-4000).  The oracle recomputes sampled rows only
+narrow model, prompts 2000-2600).  The oracle recomputes sampled rows only
 (its cost is ~0.5 GMAC per wide token).
 """
 import numpy as np
@@ -46,7 +46,7 @@ INF = float("inf")
 CASES = {
     "wide": (64, (520, 1100), (0,)),
     "longattn": (64, (520, 1100), (0, -1)),
-    "dsr1attn": (64, (2000, 4000), (8,)),
+    "dsr1attn": (64, (2000, 2600), (0,)),
 }
 
 
