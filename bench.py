@@ -694,7 +694,20 @@ def cpu_baseline(args, shp, tau):
     return out
 
 
+# tau100 the GPU arm calibrated on this workload's window (profiles/r02_bench_line.json
+# arms.tau): the reference arm cannot calibrate (that needs hundreds of oracle forwards)
+REF_TAU = 0.0809
+
+
 def run_reference(args):
+    """The oracle as it stands on the host cores, on the GPU arm's workload:
+    the protected request (row 0) decoded with the oracle's batch-shaped plan
+    of the bench batch and the GPU arm's calibrated tau100 (the verifier runs
+    on the steps whose margin is below it).  Bounded sample: one row of the
+    batch (the oracle decodes rows independently) after an 8-token prefill --
+    a prefill of the GPU arm's context (615 tokens) would take ~40 min of 8B
+    oracle forwards; the decode step's oracle cost is dominated by the weight
+    GEMVs (15 GMAC per token), attention over 640 keys adds ~1%."""
     ws, rank, _ = _dist()
     if rank != 0:
         return None
@@ -703,31 +716,35 @@ def run_reference(args):
     cores = len(os.sched_getaffinity(0))
     os.environ["OMP_NUM_THREADS"] = str(cores)
     import oracle
-    tau = args.tau if args.tau is not None else 0.0  # the GPU arm's calibrated tau100 is 0 on this config
+    tau = args.tau if args.tau is not None else REF_TAU
     m = oracle.Model(shp)
     p = [int(t) for t in np.random.default_rng(7).integers(0, shp["vocab"], 8)]
     st = oracle.State(m, 1, 8 + args.steps + args.warmup + 2)
     det = oracle.det_sched()
     st.prefill(0, p, det)
+    fast = oracle.fast_sched(args.batch)
     for _ in range(args.warmup):
-        st.step([0], [1], tau, oracle.fast_sched(1), det)
+        st.step([0], [1], tau, fast, det)
     t0 = time.time()
+    trig = 0
     for _ in range(args.steps):
-        st.step([0], [1], tau, oracle.fast_sched(1), det)
+        trig += st.step([0], [1], tau, fast, det)["n_trig"]
     dt = time.time() - t0
     v = args.steps / dt
+    sample = (f"the protected request (row 0 of the {args.batch}-row batch, the oracle's batch-{args.batch} "
+              f"reduction plan), {args.steps} timed MarginGate steps at tau={tau:.4g} ({trig} verifier runs) "
+              f"after an 8-token prefill; the GPU arm's context 615..640 is not prefilled here (~40 min of "
+              f"oracle forwards; the step cost is dominated by the 15 GMAC of weight GEMVs, attention adds ~1%)")
     return {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "tok/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": f"{args.model}-shaped {args.workload} decode, batch {args.batch}/GPU, "
-                                   f"protected={args.protected}, tau={tau}",
+                                   f"protected=one, tau={tau:.4g} (the GPU arm's tau100)",
                        "model": args.model, "global_batch": args.batch, "parallelism": "dp1 (rank 0 only)",
-                       "tau": tau, "protected": args.protected,
-                       "sample": f"one row of the {args.batch}-row batch per step (the oracle decodes rows "
-                                 "independently; batch-shaped reduction plan of batch 1), 8-token prefill"},
+                       "tau": tau, "protected": "one", "sample": sample},
             "cpu_baseline": {"value": round(v, 5), "unit": "tok/s", "cores": cores, "kind": "oracle",
-                             "sample": "one row of the batch per step (batch 1), 8-token prefill"},
+                             "sample": sample},
             "e2e": {"value": round(v, 5), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
