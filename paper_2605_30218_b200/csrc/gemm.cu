@@ -37,6 +37,9 @@
 #include "gemm_tc.cuh"
 #include "kernels.h"
 
+#ifndef MG_EPI_STORE
+#define MG_EPI_STORE 1  // 1: partials via a shared-memory transpose and float4 stores; 0: scalar stores
+#endif
 #ifndef MG_EPI_WAIT
 #define MG_EPI_WAIT mbar_wait  // accumulator-ready wait of the epilogue poller
 #endif
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(192, 1)
     if (ctr && lane == 0) ctr[2] = (long long)globaltimer();
   } else {  // ---- epilogue warps 2..5: TMEM lanes 32*(warp%4) ..
     __shared__ Top2 s_t2[4][16];         // fused top-2: per-warp results of one 16-token chunk
-    __shared__ float s_val[4][16 * 33];  // fused top-2: per-warp [token][row] transpose (padded)
+    __shared__ __align__(16) float s_val[4][16 * 33];  // per-warp [token][row] transposes (top-2 padded; stores dense)
     griddep_wait();
     const int q = warp & 3;
     int j = 0;
@@ -224,11 +227,30 @@ __global__ void __launch_bounds__(192, 1)
           continue;
         }
         if (!(g.dbg & 2)) {
+#if MG_EPI_STORE == 1
+          // transpose the warp's 32 rows x 16 tokens through shared memory and
+          // write each token's 32 consecutive features as float4s: 4 store
+          // instructions of 4 full 128-byte lines each instead of 16 scalar ones
+          float* sv = s_val[q];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) sv[i * 32 + lane] = __uint_as_float(r[i]);
+          __syncwarp();
+          const int n0 = pc.mt * C::BM + q * 32;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int idx = k * 32 + lane, i = idx >> 3, p4 = (idx & 7) * 4;
+            const int t = t0 + c0 + i;
+            if (t < g.T)
+              *reinterpret_cast<float4*>(o + (size_t)t * g.N + n0 + p4) = *reinterpret_cast<const float4*>(sv + i * 32 + p4);
+          }
+          __syncwarp();
+#else
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int t = t0 + c0 + i;
             if (t < g.T) o[(size_t)t * g.N + n] = __uint_as_float(r[i]);
           }
+#endif
         }
       }
       tc_fence_before();
