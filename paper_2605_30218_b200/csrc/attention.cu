@@ -169,18 +169,62 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
   v_sl = k_sl;
   v_row = k_row;
   int ik = 0, iv = 0;  // blocks issued per stream
+  uint16_t* kvn = reinterpret_cast<uint16_t*>(sm + C::KVN_OFF);
+  const bool has_new = a.fuse_qkv && sp == n_sp - 1;  // this CTA holds key n - 1
+
+  // fused QKV epilogue (the same arithmetic as k_epi_qkv): q rows
+  // of the G heads into the swizzled Q tile; the new K/V column (RoPE on K) into
+  // kvn and appended to the cache at position p = n - 1.  Items
+  // (one rotation pair each) are taken QI per thread per round; everything that
+  // does not depend on the QKV GEMM (position, bias, RoPE factors, the cache
+  // address) is loaded first -- on the fast path before griddepcontrol.wait --
+  // and the partial-slot loads of all QI items are issued together after it,
+  // so a round costs one L2 round trip instead of one per item and operand.
+  constexpr int h2 = HD / 2, QI = RK + RV > 2 ? 2 : 3;  // 2 keeps the deeper-ring variants spill-free
+  struct QItem {
+    int f1, g, i;  // feature of the pair's first half; q head in group (isq) or 0 = K, 1 = V; pair index
+    bool isq, live;
+    float ba, bb, c, sn;
+    uint16_t* dst;
+  };
+  const int nq = G * h2, nitems = (a.fuse_qkv && !(a.dbg & 1)) ? nq + (has_new ? 2 * h2 : 0) : 0;
+  int p = 0;
+  QItem qi[QI];
+  auto prep = [&](int base) {
+#pragma unroll
+    for (int j = 0; j < QI; ++j) {
+      QItem& it = qi[j];
+      const int w = base + j * kAtThreads + threadIdx.x;
+      it.live = w < nitems;
+      if (!it.live) continue;
+      it.isq = w < nq;
+      it.g = it.isq ? w / h2 : (w - nq) / h2;
+      it.i = (it.isq ? w : w - nq) % h2;
+      const int h = it.isq ? kvh * G + it.g : H + it.g * a.KV + kvh;
+      it.f1 = h * HD + it.i;
+      it.ba = a.bias ? bf2f(a.bias[it.f1]) : 0.f;
+      it.bb = a.bias ? bf2f(a.bias[it.f1 + h2]) : 0.f;
+      if (it.isq || it.g == 0) {
+        it.c = a.rcos[(size_t)p * h2 + it.i];
+        it.sn = a.rsin[(size_t)p * h2 + it.i];
+      }
+      it.dst = it.isq ? nullptr : cache_ptr(cview, a.slot[t], p, it.g, kvh);
+    }
+  };
+  if (nitems) p = a.pos[t];
   if (a.prewait) {
     // PDL: blocks whose keys all precede this step's appended column (n - 1)
     // were written by earlier steps -- fetched before griddepcontrol.wait
     auto early = [&](int i) { return lo + 16 * (warp + 4 * i) + 16 <= n - 1; };
     for (; ik < RK && ik < nbw && early(ik); ++ik) issue_k(ik);
     for (; iv < RV && iv < nbw && early(iv); ++iv) issue_v(iv);
+    if (nitems) prep(0);
     griddep();
+  } else if (nitems) {
+    prep(0);
   }
   for (; ik < RK && ik < nbw; ++ik) issue_k(ik);  // the remaining first blocks (after the wait)
   for (; iv < RV && iv < nbw; ++iv) issue_v(iv);
-  uint16_t* kvn = reinterpret_cast<uint16_t*>(sm + C::KVN_OFF);
-  const bool has_new = a.fuse_qkv && sp == n_sp - 1;  // this CTA holds key n - 1
   if (!a.fuse_qkv) {
     if (warp == 0 && lane == 0) {
       mbar_expect_tx(&bars[0], C::BLK);
@@ -189,45 +233,61 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
         tma_load_3d(sm + C::Q_OFF + h * 2048, &a.qmap, &bars[0], 64 * h, kvh * G, t + a.q_row0);
     }
   } else {
-    // QKV epilogue (the same arithmetic as k_epi_qkv): q rows of
-    // the G heads into the swizzled Q tile; the new K/V column (RoPE on K) into
-    // kvn and appended to the cache at position p = n - 1
-    constexpr int h2 = HD / 2;
     const int NQKV = (H + 2 * a.KV) * HD;
     const size_t stride = (size_t)(a.part_T ? a.part_T : a.T) * NQKV, row = (size_t)t * NQKV;
-    const int p = a.pos[t];
-    const int nq = G * h2, nitems = nq + (has_new ? 2 * h2 : 0);
-    for (int w = threadIdx.x; w < nitems; w += kAtThreads) {
-      const bool isq = w < nq;
-      const int g = isq ? w / h2 : (w - nq) / h2;  // q: head in group; k/v: 0 = K, 1 = V
-      const int i = (isq ? w : w - nq) % h2;
-      const int h = isq ? kvh * G + g : H + g * a.KV + kvh;
-      const int f1 = h * HD + i, f2 = f1 + h2;
-      float x = sum_splits(a.qkv_part, part_count(a.qkv_ps, f1), stride, row + f1);
-      float y = sum_splits(a.qkv_part, part_count(a.qkv_ps, f2), stride, row + f2);
-      if (a.bias) {
-        x = __fadd_rn(x, bf2f(a.bias[f1]));
-        y = __fadd_rn(y, bf2f(a.bias[f2]));
+    for (int base = 0; base < nitems; base += QI * kAtThreads) {
+      if (base) prep(base);
+      // all slot loads of the round first (<= 8 per operand, predicated), then
+      // the sums in slot (= k) order -- sum_splits' arithmetic
+      float vx[QI][8], vy[QI][8];
+      int S[QI];
+#pragma unroll
+      for (int j = 0; j < QI; ++j) {
+        S[j] = qi[j].live ? part_count(a.qkv_ps, qi[j].f1) : 0;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          vx[j][s] = s < S[j] ? __ldcg(a.qkv_part + (size_t)s * stride + row + qi[j].f1) : 0.f;
+          vy[j][s] = s < S[j] ? __ldcg(a.qkv_part + (size_t)s * stride + row + qi[j].f1 + h2) : 0.f;
+        }
       }
-      uint16_t oa, ob;
-      if (isq || g == 0) {  // RoPE on q and k
-        const float c = a.rcos[(size_t)p * h2 + i], sn = a.rsin[(size_t)p * h2 + i];
-        oa = f2bf(__fsub_rn(__fmul_rn(x, c), __fmul_rn(y, sn)));
-        ob = f2bf(__fadd_rn(__fmul_rn(y, c), __fmul_rn(x, sn)));
-      } else {
-        oa = f2bf(x);
-        ob = f2bf(y);
-      }
-      if (isq) {
-        uint8_t* qt = sm + C::Q_OFF;
-        *reinterpret_cast<uint16_t*>(qt + swz(g, i) + (i & 7) * 2) = oa;
-        *reinterpret_cast<uint16_t*>(qt + swz(g, i + h2) + ((i + h2) & 7) * 2) = ob;
-      } else {
-        kvn[g * HD + i] = oa;
-        kvn[g * HD + i + h2] = ob;
-        uint16_t* dst = cache_ptr(cview, a.slot[t], p, g, kvh);
-        dst[i] = oa;
-        dst[i + h2] = ob;
+#pragma unroll
+      for (int j = 0; j < QI; ++j) {
+        const QItem& it = qi[j];
+        if (!it.live) continue;
+        float x = vx[j][0], y = vy[j][0];
+#pragma unroll
+        for (int s = 1; s < 8; ++s)
+          if (s < S[j]) {
+            x = __fadd_rn(x, vx[j][s]);
+            y = __fadd_rn(y, vy[j][s]);
+          }
+        for (int s = 8; s < S[j]; ++s) {
+          x = __fadd_rn(x, __ldcg(a.qkv_part + (size_t)s * stride + row + it.f1));
+          y = __fadd_rn(y, __ldcg(a.qkv_part + (size_t)s * stride + row + it.f1 + h2));
+        }
+        if (a.bias) {
+          x = __fadd_rn(x, it.ba);
+          y = __fadd_rn(y, it.bb);
+        }
+        uint16_t oa, ob;
+        if (it.isq || it.g == 0) {  // RoPE on q and k
+          oa = f2bf(__fsub_rn(__fmul_rn(x, it.c), __fmul_rn(y, it.sn)));
+          ob = f2bf(__fadd_rn(__fmul_rn(y, it.c), __fmul_rn(x, it.sn)));
+        } else {
+          oa = f2bf(x);
+          ob = f2bf(y);
+        }
+        const int i = it.i;
+        if (it.isq) {
+          uint8_t* qt = sm + C::Q_OFF;
+          *reinterpret_cast<uint16_t*>(qt + swz(it.g, i) + (i & 7) * 2) = oa;
+          *reinterpret_cast<uint16_t*>(qt + swz(it.g, i + h2) + ((i + h2) & 7) * 2) = ob;
+        } else {
+          kvn[it.g * HD + i] = oa;
+          kvn[it.g * HD + i + h2] = ob;
+          it.dst[i] = oa;
+          it.dst[i + h2] = ob;
+        }
       }
     }
     __syncthreads();
@@ -256,6 +316,20 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
     const bool new_blk = has_new && lo + 16 * (warp + 4 * i) + 16 >= n;  // holds key n - 1
     const int rr_new = n - 1 - (lo + 16 * (warp + 4 * i));
     mbar_wait(&kfull[i % RK], (uint32_t)((i / RK) & 1));
+    if (a.dbg & 2) {  // microbenchmark: stream only
+      __syncwarp();
+      if (i + RK < nbw) {
+        if (((i + RK) & 31) == 0) coords(i + RK, k_sl, k_row);
+        issue_k(i + RK);
+      }
+      mbar_wait(&vfull[i % RV], (uint32_t)((i / RV) & 1));
+      __syncwarp();
+      if (i + RV < nbw) {
+        if (((i + RV) & 31) == 0) coords(i + RV, v_sl, v_row);
+        issue_v(i + RV);
+      }
+      continue;
+    }
     if (new_blk) {  // patch the new K row
       for (int e = lane; e < HD / 8; e += 32)
         *reinterpret_cast<uint4*>(kst + swz(rr_new, e * 8)) = *reinterpret_cast<const uint4*>(kvn + e * 8);
@@ -356,6 +430,7 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
   l1 = __fadd_rn(l1, __shfl_xor_sync(0xffffffffu, l1, 2));
 
   // ---- combine the 4 warps (streams) in warp order
+  if (a.dbg & 4) return;
   __syncthreads();  // every ring consumed: the scratch may alias them
   float* X = reinterpret_cast<float*>(sm + C::RING_OFF);
   if ((lane & 3) == 0) {

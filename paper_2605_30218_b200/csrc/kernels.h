@@ -148,6 +148,10 @@ struct AttnArgs {
   int32_t split_keys1;
   CacheView cache1;
   CUtensorMap kvmap1;
+  // microbenchmark knobs (scripts/attn_dbg.cu; 0 in the library): 1 skip the
+  // fused QKV epilogue's arithmetic, 2 skip QK^T / softmax / PV (stream only),
+  // 4 skip the warp combine and the output stores
+  int32_t dbg;
 };
 bool make_tmap_3d(CUtensorMap* m, const void* base, int d0, int64_t d1, int64_t d2, int box1);
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st);

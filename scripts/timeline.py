@@ -45,8 +45,17 @@ print(f"{len(ks)} kernels in {steps} steps; span {(ks[-1]['ts'] + ks[-1]['dur'] 
 # so start-based durations overlap)
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
 prev_end = None
+# GEMMs are labelled by their place in the step: 4 per layer (qkv, o, gate/up,
+# down), then the LM head; a step starts at its k_embed
+gi, gname = 0, ("qkv", "o", "gu", "down")
+nl = shp["n_layers"]
 for e in ks:
     n = e["name"].split("(")[0].replace("void ", "")[:34]
+    if "k_embed" in n:
+        gi = 0
+    if "k_gemm_tc" in n:
+        n = f"{n[:26]} {gname[gi % 4] if gi < 4 * nl else 'lm'}"
+        gi += 1
     end = e["ts"] + e["dur"]
     a = agg[n]
     a[0] += 1
