@@ -1,10 +1,10 @@
 // epilogue.cuh -- device-side GEMM epilogue math shared by the standalone
-// elementwise kernels (elementwise.cu) and the persistent layer chain
-// (chain.cu): split-K partial sums in k order, the RMSNorm pieces, SwiGLU and
-// the QKV bias + RoPE + cache append.  Every rounding point follows DESIGN.md
+// elementwise kernels (elementwise.cu), the attention kernel's fused QKV
+// epilogue and the GEMM's fused prologue (gemm.cu): split-K partial sums in k
+// order, the RMSNorm pieces, SwiGLU and the QKV bias + RoPE + cache append.  Every rounding point follows DESIGN.md
 // 3.3 (explicit __fadd_rn/__fmul_rn/__fdiv_rn, bf16 round-to-nearest-even).
-// Partials are read with ld.global.cg: in the chain they were written by other
-// CTAs of the same grid, and no L1 line may be trusted.
+// Partials are read with ld.global.cg (L2): other CTAs wrote them, so no L1
+// line may be trusted.
 #pragma once
 #include "common.cuh"
 #include "kernels.h"
@@ -227,37 +227,6 @@ __device__ __forceinline__ QkvPair qkv_prep(const QkvArgs& a, int t, int h, int 
       r.dst = a.paged ? cache_ptr(a.cache, a.slot[t], p, kvsel, kh)  // tentative append of column p
                       : (kvsel ? a.vd : a.kd) + (size_t)t * a.KV * a.hd + kh * a.hd;
     }
-  }
-  return r;
-}
-// the same with the token's position and KV page already known (staged in
-// shared memory by the layer chain): no dependent global loads
-__device__ __forceinline__ QkvPair qkv_prep_staged(const QkvArgs& a, int t, int h, int i, int p, int page) {
-  QkvPair r;
-  const int h2 = a.hd / 2;
-  const int NQKV = (a.H + 2 * a.KV) * a.hd;
-  r.f1 = h * a.hd + i;
-  r.f2 = r.f1 + h2;
-  r.row = (size_t)t * NQKV;
-  r.ba = r.bb = 0.f;
-  r.c = 1.f;
-  r.sn = 0.f;
-  if (a.bias) {
-    r.ba = bf2f(a.bias[r.f1]);
-    r.bb = bf2f(a.bias[r.f2]);
-  }
-  if (h < a.H + a.KV) {
-    r.c = a.rcos[(size_t)p * h2 + i];
-    r.sn = a.rsin[(size_t)p * h2 + i];
-  }
-  if (h < a.H) {
-    r.dst = a.q + (size_t)t * a.H * a.hd + h * a.hd;
-  } else {
-    const int kvsel = h < a.H + a.KV ? 0 : 1;
-    const int kh = h - a.H - kvsel * a.KV;
-    const CacheView& c = a.cache;
-    r.dst = c.pool + ((((size_t)c.layer * c.n_pages + page) * 2 + kvsel) * c.kv + kh) * (size_t)c.page_size * c.hd +
-            (size_t)(p % c.page_size) * c.hd;
   }
   return r;
 }

@@ -1,5 +1,5 @@
 // gemm_tc.cuh -- pieces shared by the tcgen05 weight-streaming kernels
-// (k_gemm_tc in gemm.cu, the persistent layer chain k_chain in chain.cu):
+// (k_gemm_tc in gemm.cu, scripts/gemm_*.cu microbenchmarks):
 // the smem/pipeline configuration, the stream-K piece iterator and the
 // per-stage MMA issue.
 #pragma once
@@ -64,15 +64,6 @@ struct PieceIter {
   int v, i, tt, u;
   __device__ explicit PieceIter(const GemmArgs& g, int KB_) {
     KB = KB_; n_m = g.n_m; n_t = g.n_t; S = g.splits; G = g.G; units = g.units;
-    W = (long long)n_m * KB;
-    u = blockIdx.x;
-    v = (int)blockIdx.x - (int)gridDim.x;
-    w = w1 = 0;
-    i = tt = 0;
-  }
-  // stream-K over G virtual CTAs per token tile (the layer chain)
-  __device__ PieceIter(int KB_, int n_m_, int n_t_, int G_) {
-    KB = KB_; n_m = n_m_; n_t = n_t_; S = 1; G = G_; units = n_m * n_t;
     W = (long long)n_m * KB;
     u = blockIdx.x;
     v = (int)blockIdx.x - (int)gridDim.x;
