@@ -1,8 +1,10 @@
 """Kernel timeline of pipelined decode steps via torch.profiler (CUPTI) -- diagnostic only.
 
-usage: python scripts/timeline.py [model] [B] [ctx] [tau] [steps] > summary
+usage: python scripts/timeline.py [model] [B] [ctx] [tau] [steps] [passes] > summary
 Prints per kernel class: count, mean duration, and the mean gap between the
 end of the previous kernel and the start of this one (the pipeline bubble).
+passes = 2 (tau = inf, every row protected: a fast forward then a verifier
+forward per step) labels the GEMMs and attention kernels F / V by forward.
 """
 import collections
 import json
@@ -21,6 +23,7 @@ B = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 ctx = int(sys.argv[3]) if len(sys.argv) > 3 else 384
 tau = float(sys.argv[4]) if len(sys.argv) > 4 else 0.0
 steps = int(sys.argv[5]) if len(sys.argv) > 5 else 3
+passes = int(sys.argv[6]) if len(sys.argv) > 6 else 1
 shp = inputs.shape(model)
 eng = Engine(shp, max_batch=B, max_seq=ctx + 64, page_size=64)
 for i, p in enumerate(inputs.prompts(B, ctx, shp["vocab"])):
@@ -49,13 +52,18 @@ prev_end = None
 # down), then the LM head; a step starts at its k_embed
 gi, gname = 0, ("qkv", "o", "gu", "down")
 nl = shp["n_layers"]
+ne = -1
 for e in ks:
     n = e["name"].split("(")[0].replace("void ", "")[:34]
     if "k_embed" in n:
         gi = 0
+        ne += 1
+    tag = ("F", "V")[ne % 2] + " " if passes == 2 else ""
     if "k_gemm_tc" in n:
-        n = f"{n[:26]} {gname[gi % 4] if gi < 4 * nl else 'lm'}"
+        n = f"{tag}{n[:26]} {gname[gi % 4] if gi < 4 * nl else 'lm'}"
         gi += 1
+    elif "k_attn" in n:
+        n = f"{tag}{n}"
     end = e["ts"] + e["dur"]
     a = agg[n]
     a[0] += 1
