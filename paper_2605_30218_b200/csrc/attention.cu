@@ -515,13 +515,16 @@ static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
                   a);
 }
 
-// ring depths (RK, RV): (2, 2) while the grid fits ~3 CTAs per SM; else
-// (1, 1) (4 CTAs per SM, 40 KB each at hd 128).  (2, 1) -- the K stream two
-// blocks ahead at 55 KB per CTA, still 4 per SM -- measured the same step time
-// at B = 64 / 8 (llama8b, ctx 384: 4.34 vs 4.33 ms, 3.48 vs 3.49 ms), so the
-// smaller footprint stays the default.  MG_ATTN_RING=11|21|22 forces it
-// (measurement only).
-static int g_attn_ring = 0;
+// ring depths (RK, RV): (4, 4) when the grid has at most one CTA per SM (small
+// batches and the verifier's few rows: a warp's blocks are in flight together;
+// 1% faster steps at B = 1 / 8, profiles/r02_ab_attn_deep_ring.txt), (2, 2)
+// while it fits ~3 CTAs per SM, else (1, 1) (4 CTAs per SM, 40 KB each at hd
+// 128).  (2, 1) -- the K stream two blocks ahead at 55 KB per CTA, still 4 per
+// SM -- measured the same step time at B = 64 / 8 (llama8b, ctx 384: 4.34 vs
+// 4.33 ms, 3.48 vs 3.49 ms), so the smaller footprint stays the default.
+// MG_ATTN_RING=11|21|22|44|66 forces a ring, MG_ATTN_DEEP=0|44|66 sets the
+// small-grid one (measurement only).  Ring depth changes timing only.
+static int g_attn_ring = 0, g_attn_deep = 44;
 
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st) {
   if (a.H % a.KV || a.H / a.KV > 16 || !a.counter || a.split_keys < 64 || a.split_keys % 64 || a.n_splits < 1)
@@ -530,16 +533,31 @@ cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st) {
   if (!g_attn_ring) {
     const char* s = getenv("MG_ATTN_RING");
     const int v = s ? atoi(s) : 0;
-    g_attn_ring = (v == 11 || v == 21 || v == 22) ? v : -1;
+    g_attn_ring = (v == 11 || v == 21 || v == 22 || v == 44 || v == 66) ? v : -1;
+    const char* d = getenv("MG_ATTN_DEEP");  // ring of grids with <= one CTA per SM (44 / 66; 0 = the 22 rule)
+    if (d) g_attn_deep = atoi(d);
   }
   const long ctas = (long)a.T * a.KV * a.n_splits;
-  const int R = g_attn_ring > 0 ? g_attn_ring : (ctas <= 3L * num_sms() ? 22 : 11);
-  if (a.hd == 128)
-    return R == 22 ? launch_attn_t<128, 2, 2>(a, st)
-                   : (R == 21 ? launch_attn_t<128, 2, 1>(a, st) : launch_attn_t<128, 1, 1>(a, st));
-  if (a.hd == 64)
-    return R == 22 ? launch_attn_t<64, 2, 2>(a, st)
-                   : (R == 21 ? launch_attn_t<64, 2, 1>(a, st) : launch_attn_t<64, 1, 1>(a, st));
+  const int R = g_attn_ring > 0 ? g_attn_ring
+                                : (ctas <= num_sms() && g_attn_deep ? g_attn_deep : (ctas <= 3L * num_sms() ? 22 : 11));
+  if (a.hd == 128) {
+    switch (R) {
+      case 66: return launch_attn_t<128, 6, 6>(a, st);
+      case 44: return launch_attn_t<128, 4, 4>(a, st);
+      case 22: return launch_attn_t<128, 2, 2>(a, st);
+      case 21: return launch_attn_t<128, 2, 1>(a, st);
+      default: return launch_attn_t<128, 1, 1>(a, st);
+    }
+  }
+  if (a.hd == 64) {
+    switch (R) {
+      case 66: return launch_attn_t<64, 6, 6>(a, st);
+      case 44: return launch_attn_t<64, 4, 4>(a, st);
+      case 22: return launch_attn_t<64, 2, 2>(a, st);
+      case 21: return launch_attn_t<64, 2, 1>(a, st);
+      default: return launch_attn_t<64, 1, 1>(a, st);
+    }
+  }
   return cudaErrorInvalidValue;
 }
 
