@@ -75,6 +75,22 @@ def test_bf16_random_and_idempotent(orc):
     assert np.array_equal(_oracle_bf16(orc, back), got)  # round(round(x)) == round(x)
 
 
+def test_bf16_exhaustive(orc, tmp_path):
+    """All 2^32 fp32 bit patterns (test plan item 1) through the
+    oracle's conversion against tests/bf16_exhaustive.c, which rounds by exact
+    fp64 distance to the two bf16 neighbours (not the oracle's add-and-
+    truncate); a C loop over liboracle.so, ~5 s on 8 cores."""
+    import os
+    import subprocess
+    lib = orc.lib()._name
+    src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "bf16_exhaustive.c")
+    exe = str(tmp_path / "bf16_exhaustive")
+    subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-Wall", src, lib,
+                           "-Wl,-rpath," + os.path.dirname(lib), "-lm", "-o", exe])
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "checked 4294967296 mismatches 0" in out.stdout, out.stdout
+
+
 def test_bf16_specials(orc):
     b = _oracle_bf16(orc, np.array([np.inf, -np.inf, np.nan, 3.4e38, -3.4e38], np.float32))
     f = orc.bf16_to_f32(b)
