@@ -62,6 +62,12 @@ mg_status mgd_qkv_epilogue(const float* part, int32_t splits, const uint16_t* bi
 mg_status mgd_attention(const uint16_t* q, const uint16_t* K, const uint16_t* V, const int32_t* n_keys, int32_t T,
                         int32_t H, int32_t KV, int32_t hd, int32_t key_stride, int32_t split_keys, uint16_t* o,
                         void* stream);
+/* The same with `streams` (2 or 4) round-robin key streams per split: the
+ * fast path runs 2 streams when its grid exceeds one wave of 4-warp CTAs
+ * (DESIGN.md 7); 4 = mgd_attention. */
+mg_status mgd_attention_streams(const uint16_t* q, const uint16_t* K, const uint16_t* V, const int32_t* n_keys,
+                                int32_t T, int32_t H, int32_t KV, int32_t hd, int32_t key_stride, int32_t split_keys,
+                                int32_t streams, uint16_t* o, void* stream);
 
 /* out[t][i] = bf16(x[t][i] + sum_s part[s][t][i]) */
 mg_status mgd_residual(const uint16_t* x, const float* part, int32_t splits, int32_t T, int32_t N, uint16_t* out,

@@ -55,8 +55,8 @@ class MgStats(C.Structure):
 # every symbol declared in include/mg.h and include/mg_debug.h
 PUBLIC_SYMBOLS = ["mg_query_sizes", "mg_init", "mg_prefill", "mg_decode_step", "mg_stats", "mg_release",
                   "mg_destroy", "mg_last_error", "mg_set_policy", "mg_verify_window"]
-DEBUG_SYMBOLS = ["mgd_gen_tensor", "mgd_rmsnorm", "mgd_gemm", "mgd_qkv_epilogue", "mgd_attention", "mgd_residual",
-                 "mgd_swiglu", "mgd_top2", "mgd_gate", "mgd_read_column", "mgd_cache_digest", "mgd_last_step",
+DEBUG_SYMBOLS = ["mgd_gen_tensor", "mgd_rmsnorm", "mgd_gemm", "mgd_qkv_epilogue", "mgd_attention",
+                 "mgd_attention_streams", "mgd_residual", "mgd_swiglu", "mgd_top2", "mgd_gate", "mgd_read_column", "mgd_cache_digest", "mgd_last_step",
                  "mgd_capture_logits", "mgd_weight", "mgd_schedule", "mgd_launch_count", "mgd_set_timing",
                  "mgd_timing", "mgd_capture_verifier_logits", "mgd_set_inject",
                  "mgd_force_schedule", "mgd_gemm_top2"]
@@ -83,6 +83,7 @@ _SIGS = {
     "mgd_gemm": [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp],
     "mgd_qkv_epilogue": [_vp, _i32, _vp, _vp, _i32, _i32, _i32, _i32, _f32, _i32, _vp, _vp, _vp, _vp],
     "mgd_attention": [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp],
+    "mgd_attention_streams": [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp],
     "mgd_residual": [_vp, _vp, _i32, _i32, _i32, _vp, _vp],
     "mgd_swiglu": [_vp, _i32, _i32, _i32, _vp, _vp],
     "mgd_top2": [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

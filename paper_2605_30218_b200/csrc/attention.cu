@@ -37,25 +37,24 @@
 
 namespace mg {
 
-constexpr int kAtThreads = 128;
 
 // Per warp: a ring of RK K blocks and a separate ring of RV V blocks, each
 // with its own mbarriers, so the K block of step i + RK is requested as soon as
 // QK^T of step i has read its stage (it streams while softmax and PV run) and
 // the V block of step i + RV as soon as PV of step i is done.
-template <int HD, int RK, int RV>
+template <int HD, int RK, int RV, int NW = 4>
 struct AtCfg {
   static constexpr int HALVES = HD / 64;
   static constexpr int BLK = HALVES * 2048;        // one 16-row tile: HALVES x [16][128 B] swizzled
   static constexpr int WRING = (RK + RV) * BLK;    // one warp's K ring then V ring
   static constexpr int XST = HD + 8;               // cross-warp scratch row stride (floats)
-  static constexpr int RING = 4 * WRING;
-  static constexpr int XG = 4 * 16 * XST * 4;      // [warp][16][XST] fp32, aliases the rings
+  static constexpr int RING = NW * WRING;
+  static constexpr int XG = NW * 16 * XST * 4;     // [warp][16][XST] fp32, aliases the rings
   static constexpr int Q_OFF = 0;
   static constexpr int RING_OFF = BLK;
   static constexpr int ML_OFF = RING_OFF + (RING > XG ? RING : XG);  // m, l: [warp][16] each
   static constexpr int KVN_OFF = ML_OFF + 2 * 64 * 4;                // fused QKV: new K and V rows [2][HD] bf16
-  static constexpr int NBAR = 1 + 4 * (RK + RV);                     // Q, then [warp][RK K | RV V]
+  static constexpr int NBAR = 1 + NW * (RK + RV);                    // Q, then [warp][RK K | RV V]
   static constexpr int BAR_OFF = KVN_OFF + 2 * HD * 2;
   static constexpr int SMEM = BAR_OFF + NBAR * 8 + 8 + 1024;         // + flag + alignment slack
 };
@@ -88,9 +87,10 @@ MG_DEV void split_pair(float e0, float e1, uint32_t& hi, uint32_t& lo) {
   lo = pack_bf2(__fsub_rn(e0, lo_bf(hi)), __fsub_rn(e1, hi_bf(hi)));
 }
 
-template <int HD, int RK, int RV>
-__global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ AttnArgs a) {
-  using C = AtCfg<HD, RK, RV>;
+template <int HD, int RK, int RV, int NW>
+__global__ void __launch_bounds__(NW * 32, 16 / NW) k_attn(const __grid_constant__ AttnArgs a) {
+  using C = AtCfg<HD, RK, RV, NW>;
+  constexpr int kAtThreads = NW * 32;  // NW streams (warps) per CTA
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
   float* s_m = reinterpret_cast<float*>(sm + C::ML_OFF);  // [warp][16]
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
   if (lo >= n) return;
   const int hi = min(n, lo + split_keys);
   const int nblk = (hi - lo + 15) >> 4;
-  const int nbw = nblk > warp ? (nblk - warp + 3) >> 2 : 0;  // blocks of this warp
+  const int nbw = nblk > warp ? (nblk - warp + NW - 1) / NW : 0;  // blocks of this warp
   const int n_sp = (n + split_keys - 1) / split_keys;
   uint8_t* kring = sm + C::RING_OFF + warp * C::WRING;
   uint8_t* vring = kring + RK * C::BLK;
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
   auto coords = [&](int base, int& o_sl, int& o_row) {
     const int i = base + lane;
     if (i < nbw) {
-      const int key0 = lo + 16 * (warp + 4 * i);
+      const int key0 = lo + 16 * (warp + NW * i);
       if (a.paged) {
         const CacheView& cv = cview;
         const int page = cv.pt[(size_t)a.slot[t] * cv.max_pages + key0 / cv.page_size];
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
   if (a.prewait) {
     // PDL: blocks whose keys all precede this step's appended column (n - 1)
     // were written by earlier steps -- fetched before griddepcontrol.wait
-    auto early = [&](int i) { return lo + 16 * (warp + 4 * i) + 16 <= n - 1; };
+    auto early = [&](int i) { return lo + 16 * (warp + NW * i) + 16 <= n - 1; };
     for (; ik < RK && ik < nbw && early(ik); ++ik) issue_k(ik);
     for (; iv < RV && iv < nbw && early(iv); ++iv) issue_v(iv);
     if (nitems) prep(0);
@@ -312,9 +312,9 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
     uint8_t* kst = kring + (i % RK) * C::BLK;
     uint8_t* vst = vring + (i % RV) * C::BLK;
     const uint32_t kb = smem_u32(kst), vb = smem_u32(vst);
-    const int valid = min(16, hi - (lo + 16 * (warp + 4 * i)));
-    const bool new_blk = has_new && lo + 16 * (warp + 4 * i) + 16 >= n;  // holds key n - 1
-    const int rr_new = n - 1 - (lo + 16 * (warp + 4 * i));
+    const int valid = min(16, hi - (lo + 16 * (warp + NW * i)));
+    const bool new_blk = has_new && lo + 16 * (warp + NW * i) + 16 >= n;  // holds key n - 1
+    const int rr_new = n - 1 - (lo + 16 * (warp + NW * i));
     mbar_wait(&kfull[i % RK], (uint32_t)((i / RK) & 1));
     if (a.dbg & 2) {  // microbenchmark: stream only
       __syncwarp();
@@ -452,10 +452,10 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
     const int g = e / HD, d = e % HD;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, s_m[w * 16 + g]);
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, s_m[w * 16 + g]);
     float L = 0.f, A = 0.f;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < NW; ++w) {
       const float wt = expf(__fsub_rn(s_m[w * 16 + g], M));
       L = __fadd_rn(L, __fmul_rn(s_l[w * 16 + g], wt));
       A = __fadd_rn(A, __fmul_rn(X[(w * 16 + g) * C::XST + d], wt));
@@ -502,17 +502,17 @@ __global__ void __launch_bounds__(kAtThreads, 4) k_attn(const __grid_constant__ 
   }
 }
 
-template <int HD, int RK, int RV>
+template <int HD, int RK, int RV, int NW = 4>
 static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_attn<HD, RK, RV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         AtCfg<HD, RK, RV>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_attn<HD, RK, RV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         AtCfg<HD, RK, RV, NW>::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_k(k_attn<HD, RK, RV>, dim3(a.T, a.KV, a.n_splits), dim3(kAtThreads), AtCfg<HD, RK, RV>::SMEM, st,
-                  a);
+  return launch_k(k_attn<HD, RK, RV, NW>, dim3(a.T, a.KV, a.n_splits), dim3(NW * 32), AtCfg<HD, RK, RV, NW>::SMEM,
+                  st, a);
 }
 
 // ring depths (RK, RV): (4, 4) when the grid has at most one CTA per SM (small
@@ -524,22 +524,35 @@ static cudaError_t launch_attn_t(const AttnArgs& a, cudaStream_t st) {
 // 4.33 ms, 3.48 vs 3.49 ms), so the smaller footprint stays the default.
 // MG_ATTN_RING=11|21|22|44|66 forces a ring, MG_ATTN_DEEP=0|44|66 sets the
 // small-grid one (measurement only).  Ring depth changes timing only.
-static int g_attn_ring = 0, g_attn_deep = 44;
+static int g_attn_ring = 0, g_attn_deep = 44, g_attn_nw2 = 1;
 
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st) {
   if (a.H % a.KV || a.H / a.KV > 16 || !a.counter || a.split_keys < 64 || a.split_keys % 64 || a.n_splits < 1)
     return cudaErrorInvalidValue;
   if (a.T1 > 0 && a.T1 < a.T && (a.split_keys1 < 64 || a.split_keys1 % 64)) return cudaErrorInvalidValue;
+  if (a.streams != 0 && a.streams != 2 && a.streams != 4) return cudaErrorInvalidValue;
   if (!g_attn_ring) {
     const char* s = getenv("MG_ATTN_RING");
     const int v = s ? atoi(s) : 0;
     g_attn_ring = (v == 11 || v == 21 || v == 22 || v == 44 || v == 66) ? v : -1;
     const char* d = getenv("MG_ATTN_DEEP");  // ring of grids with <= one CTA per SM (44 / 66; 0 = the 22 rule)
     if (d) g_attn_deep = atoi(d);
+    const char* n2 = getenv("MG_ATTN_NW2");  // 0: always 4 streams (measurement)
+    if (n2) g_attn_nw2 = atoi(n2);
   }
   const long ctas = (long)a.T * a.KV * a.n_splits;
   const int R = g_attn_ring > 0 ? g_attn_ring
                                 : (ctas <= num_sms() && g_attn_deep ? g_attn_deep : (ctas <= 3L * num_sms() ? 22 : 11));
+  // The fast path (one token group, batch-shaped arithmetic anyway) with more
+  // CTAs than one wave of 4-warp CTAs holds runs 2-warp CTAs (2 key streams, 8
+  // CTAs per SM), which keeps it in one wave: 1-1.5% faster steps at B = 96 /
+  // 128 (profiles/r02_ab_attn_two_streams.txt).  The verifier (pinned
+  // arithmetic, A14) and mixed launches always take 4 streams.
+  if (a.streams == 2 || (a.streams == 0 && g_attn_nw2 && a.prewait && (a.T1 == 0 || a.T1 >= a.T) &&
+                         ctas > 4L * num_sms() && g_attn_ring <= 0)) {
+    if (a.hd == 128) return launch_attn_t<128, 1, 1, 2>(a, st);
+    if (a.hd == 64) return launch_attn_t<64, 1, 1, 2>(a, st);
+  }
   if (a.hd == 128) {
     switch (R) {
       case 66: return launch_attn_t<128, 6, 6>(a, st);

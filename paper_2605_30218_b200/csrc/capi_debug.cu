@@ -122,8 +122,15 @@ mg_status mgd_qkv_epilogue(const float* part, int32_t splits, const uint16_t* bi
 mg_status mgd_attention(const uint16_t* q, const uint16_t* K, const uint16_t* V, const int32_t* n_keys, int32_t T,
                         int32_t H, int32_t KVh, int32_t hd, int32_t key_stride, int32_t split_keys, uint16_t* o,
                         void* stream) {
+  return mgd_attention_streams(q, K, V, n_keys, T, H, KVh, hd, key_stride, split_keys, 4, o, stream);
+}
+
+mg_status mgd_attention_streams(const uint16_t* q, const uint16_t* K, const uint16_t* V, const int32_t* n_keys,
+                                int32_t T, int32_t H, int32_t KVh, int32_t hd, int32_t key_stride, int32_t split_keys,
+                                int32_t streams, uint16_t* o, void* stream) {
   if (!q || !K || !V || !n_keys || !o || T < 1 || split_keys < 64 || split_keys % 64 || key_stride < 1)
     return MG_ERR_INVALID;
+  if (streams != 2 && streams != 4) return MG_ERR_INVALID;
   if (KVh < 1 || H % KVh || H / KVh > 16) return MG_ERR_INVALID;
   const int nsp = (key_stride + split_keys - 1) / split_keys;
   float *acc = nullptr, *ml = nullptr;
@@ -137,6 +144,7 @@ mg_status mgd_attention(const uint16_t* q, const uint16_t* K, const uint16_t* V,
   a.q = q; a.paged = 0; a.n_keys = n_keys; a.Kd = K; a.Vd = V; a.key_stride = key_stride;
   a.T = T; a.H = H; a.KV = KVh; a.hd = hd; a.split_keys = split_keys; a.n_splits = nsp;
   a.part_acc = acc; a.part_ml = ml; a.counter = cnt; a.out = o;
+  a.streams = streams;
   cudaError_t e = cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
   if (make_tmap_3d(&a.qmap, q, hd, H, T, 16) && make_tmap_3d(&a.kmap, K, hd, key_stride, (int64_t)T * KVh, 16) &&

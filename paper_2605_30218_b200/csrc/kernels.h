@@ -152,6 +152,7 @@ struct AttnArgs {
   // fused QKV epilogue's arithmetic, 2 skip QK^T / softmax / PV (stream only),
   // 4 skip the warp combine and the output stores
   int32_t dbg;
+  int32_t streams;        // warps (key streams) per CTA: 0 = launch_attention's rule, 2 or 4 forced (tests)
 };
 bool make_tmap_3d(CUtensorMap* m, const void* base, int d0, int64_t d1, int64_t d2, int box1);
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t st);

@@ -95,17 +95,17 @@ def qkv_epilogue(part: np.ndarray, bias, pos, H, KV, hd, theta):
     return to_host_u16(q), to_host_u16(k), to_host_u16(v)
 
 
-def attention(q: np.ndarray, K: np.ndarray, V: np.ndarray, n_keys, split_keys: int):
+def attention(q: np.ndarray, K: np.ndarray, V: np.ndarray, n_keys, split_keys: int, streams: int = 4):
     """q [T, H, hd]; K, V [T, KV, key_stride, hd] -> o [T, H*hd] (streamed form,
-    splits of split_keys keys; include/mg_debug.h)."""
+    splits of split_keys keys, `streams` key streams per split; include/mg_debug.h)."""
     torch = _t()
     T, H, hd = q.shape
     _, KVh, stride, _ = K.shape
     qd, kd, vd = to_dev_u16(q), to_dev_u16(K), to_dev_u16(V)
     nk = torch.from_numpy(np.ascontiguousarray(n_keys, dtype=np.int32)).cuda()
     o = torch.empty((T, H * hd), dtype=torch.int16, device="cuda")
-    check(lib().mgd_attention(_p(qd), _p(kd), _p(vd), _p(nk), T, H, KVh, hd, stride, split_keys, _p(o),
-                              _stream()), None, "attention")
+    check(lib().mgd_attention_streams(_p(qd), _p(kd), _p(vd), _p(nk), T, H, KVh, hd, stride, split_keys, streams,
+                                      _p(o), _stream()), None, "attention")
     _sync()
     return to_host_u16(o)
 

@@ -217,6 +217,32 @@ def test_attention(orc, K, H, KV, hd, sk, stride, nk):
         assert ok.all(), t
 
 
+@pytest.mark.parametrize("H,KV,hd,sk,stride,nk", [
+    (32, 8, 128, 4096, 700, (1, 17, 513, 700)), (32, 8, 128, 512, 1300, (600, 1300)),
+    (28, 4, 128, 128, 700, (1, 37, 513, 700)), (4, 4, 64, 64, 700, (1, 37, 513, 700))])
+def test_attention_two_streams(orc, K, H, KV, hd, sk, stride, nk):
+    """The fast path's 2-stream CTAs (grids above one wave of 4-warp CTAs):
+    16-key blocks dealt round-robin to 2 warps instead of 4 -- another fp32
+    order of the same sums, so test_attention's derived bound against the
+    PLAIN chunked definition applies unchanged (one chunk and 512-key chunks)."""
+    rng = np.random.default_rng(H * hd + sk + stride + 2)
+    n_keys = np.array(nk, np.int32)
+    T = len(nk)
+    q = _rand(orc, rng, (T, H, hd))
+    Kc = _rand(orc, rng, (T, KV, stride, hd))
+    Vc = _rand(orc, rng, (T, KV, stride, hd))
+    o = K.attention(q, Kc, Vc, n_keys, sk, streams=2)
+    vmax = float(np.abs(_bf(orc, Vc)).max())
+    for t in range(T):
+        n = int(n_keys[t])
+        eps = (2.0 ** -15 + n * 2.0 ** -23) * vmax
+        for chunk in (0, 512):
+            plain = orc.attention(q[t], Kc[t], Vc[t], n, chunk, 1)
+            d = np.abs(_bf(orc, o[t]) - _bf(orc, plain))
+            ok = (_ulps(orc, o[t], plain) <= 1.0) | (d <= eps)
+            assert ok.all(), (t, chunk, float(_ulps(orc, o[t], plain).max()), float(d.max()), eps)
+
+
 # ------------------------------------------------------------------ a5-a7 epilogues
 def test_residual_bit_exact(orc, K):
     rng = np.random.default_rng(5)
