@@ -17,14 +17,20 @@ using namespace mg;
 
 int main(int argc, char** argv) {
   const int H = 32, KV = 8, HD = 128, PS = 64, L = 4, NQKV = (H + 2 * KV) * HD;
-  const int Bs[] = {64, 128, 64, 32, 8};
-  const int ctxs[] = {384, 384, 620, 620, 620};
+  int Bs[] = {64, 128, 64, 32, 8};
+  int ctxs[] = {384, 384, 620, 620, 620};
+  int ncfg = 5;
+  if (argc > 2) {  // one configuration: attn_dbg B ctx
+    Bs[0] = atoi(argv[1]);
+    ctxs[0] = atoi(argv[2]);
+    ncfg = 1;
+  }
   cudaStream_t st;
   cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int c = 0; c < 5; ++c) {
+  for (int c = 0; c < ncfg; ++c) {
     const int B = Bs[c], ctx = ctxs[c];
     const int max_pages = (ctx + 1 + PS - 1) / PS, n_pages = B * max_pages;
     const size_t slab = (size_t)PS * HD;  // one (page, K|V, kv head) slab
