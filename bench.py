@@ -694,16 +694,14 @@ def cpu_baseline(args, shp, tau):
     return out
 
 
-# tau100 the GPU arm calibrated on this workload's window (profiles/r02_bench_line.json
-# arms.tau): the reference arm cannot calibrate (that needs hundreds of oracle forwards)
-REF_TAU = 0.0809
-
-
 def run_reference(args):
     """The oracle as it stands on the host cores, on the GPU arm's workload:
     the protected request (row 0) decoded with the oracle's batch-shaped plan
-    of the bench batch and the GPU arm's calibrated tau100 (the verifier runs
-    on the steps whose margin is below it).  Bounded sample: one row of the
+    of the bench batch.  Its threshold is the oracle's own perturbation bound
+    (the rule the GPU arm's calibration follows): the largest
+    |logit(batch plan) - logit(pinned plan)| over the warm-up steps, measured
+    by a second oracle state teacher-forced on the same tokens; the verifier
+    runs on the steps whose margin is below it.  Bounded sample: one row of the
     batch (the oracle decodes rows independently) after an 8-token prefill --
     a prefill of the GPU arm's context (615 tokens) would take ~40 min of 8B
     oracle forwards; the decode step's oracle cost is dominated by the weight
@@ -716,15 +714,21 @@ def run_reference(args):
     cores = len(os.sched_getaffinity(0))
     os.environ["OMP_NUM_THREADS"] = str(cores)
     import oracle
-    tau = args.tau if args.tau is not None else REF_TAU
     m = oracle.Model(shp)
     p = [int(t) for t in np.random.default_rng(7).integers(0, shp["vocab"], 8)]
     st = oracle.State(m, 1, 8 + args.steps + args.warmup + 2)
     det = oracle.det_sched()
     st.prefill(0, p, det)
     fast = oracle.fast_sched(args.batch)
+    pin = oracle.State(m, 1, 8 + args.warmup + 2)   # the pinned plan on the same tokens (warm-up only)
+    pin.prefill(0, p, det)
+    eps = 0.0
     for _ in range(args.warmup):
-        st.step([0], [1], tau, fast, det)
+        ra = st.step([0], [1], 0.0, fast, det, want_logits=True)
+        rd = pin.step([0], [1], 0.0, det, det, forced_out=[int(ra["out"][0])], want_logits=True)
+        eps = max(eps, float(np.abs(ra["logits"][0] - rd["logits"][0]).max()))
+    pin.close()
+    tau = args.tau if args.tau is not None else eps
     t0 = time.time()
     trig = 0
     for _ in range(args.steps):
@@ -740,7 +744,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": f"{args.model}-shaped {args.workload} decode, batch {args.batch}/GPU, "
-                                   f"protected=one, tau={tau:.4g} (the GPU arm's tau100)",
+                                   f"protected=one, tau={tau:.4g} (the oracle's eps_pert over the warm-up)",
                        "model": args.model, "global_batch": args.batch, "parallelism": "dp1 (rank 0 only)",
                        "tau": tau, "protected": "one", "sample": sample},
             "cpu_baseline": {"value": round(v, 5), "unit": "tok/s", "cores": cores, "kind": "oracle",
