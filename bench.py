@@ -235,6 +235,7 @@ def run_gpu(args):
         if timing:
             r["tim"] = eng.timing()
             eng.set_timing(False)
+            r["tim"]["floor_us"] = _launch_floor(eng)
         if clocks:
             r["clk"] = clocks.stop()
         s1 = eng.stats()
@@ -434,6 +435,12 @@ def run_gpu(args):
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm else "fallback 6650 GB/s (B200_PROFILING.md)"
     hbm = hbm or 6650.0
     achieved = tim["gemm_bytes"] / (tim["gemm_ms"] * 1e-3) / 1e9 if tim["gemm_ms"] > 0 else None
+    # the same launches less the measured floor of an event-bracketed launch
+    # (an empty kernel of the GEMM's launch shape): what the raw per-launch
+    # figure charges to launch processing rather than to the kernel
+    floor_us = tim.get("floor_us")
+    net_ms = tim["gemm_ms"] - (floor_us or 0.0) * 1e-3 * tim["gemm_launches"]
+    achieved_net = tim["gemm_bytes"] / (net_ms * 1e-3) / 1e9 if floor_us and net_ms > 0 else None
     traffic = None
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json"))).get("bytes_per_launch")
@@ -516,6 +523,11 @@ def run_gpu(args):
                      "traffic": traffic, "kernel": "k_gemm_tc (weight-streaming GEMM class, fast path)",
                      "peak_source": peak_src, "gemm_launches": tim["gemm_launches"],
                      "gemm_us_per_launch": round(1e3 * tim["gemm_ms"] / max(tim["gemm_launches"], 1), 2),
+                     "launch_floor_us": round(floor_us, 2) if floor_us else None,
+                     "net_of_launch_floor": ({"achieved": round(achieved_net, 1), "frac": round(achieved_net / hbm, 4),
+                                              "note": "per-launch bytes / (event time - the event-bracketed launch "
+                                                      "time of an empty kernel of the GEMM's shape, mgd_launch_floor)"}
+                                             if achieved_net else None),
                      "gemm_ms_per_step": round(tim["gemm_ms"] / K, 4),
                      "attn_ms_per_step": round(tim["attn_ms"] / K, 4),
                      "fast_step_ms_timed_pass": round(tim["step_ms"] / max(tim["steps"], 1), 4),
@@ -692,6 +704,19 @@ def cpu_baseline(args, shp, tau):
                                           "sample": f"configs[0]: 8 prompts x 32 greedy tokens at batch {bs}, "
                                                     f"tau 0.3, {dtt:.2f} s"}
     return out
+
+
+def _launch_floor(eng, reps=50):
+    """Mean CUDA-event-bracketed time of an empty kernel with the fast-path
+    GEMM's launch shape (148 x 192 threads, the 64-token tile's 197744 B of
+    shared memory) on the engine's stream (include/mg_debug.h)."""
+    import ctypes as C
+
+    from paper_2605_30218_b200._lib import lib
+    us = C.c_float(0.0)
+    if lib().mgd_launch_floor(197744, reps, C.c_void_p(eng.stream.cuda_stream), C.byref(us)) != 0:
+        return None
+    return float(us.value)
 
 
 def run_reference(args):

@@ -69,6 +69,12 @@ mg_status mgd_attention_streams(const uint16_t* q, const uint16_t* K, const uint
                                 int32_t T, int32_t H, int32_t KV, int32_t hd, int32_t key_stride, int32_t split_keys,
                                 int32_t streams, uint16_t* o, void* stream);
 
+/* Measurement floor of bench.py's per-launch roofline timing: an empty kernel
+ * with the GEMM's launch shape (one CTA per SM x 192 threads, smem_bytes of
+ * dynamic shared memory) bracketed by two CUDA events on `stream`, `reps`
+ * times; *us_out = the mean bracketed time in microseconds.  Blocking. */
+mg_status mgd_launch_floor(int32_t smem_bytes, int32_t reps, void* stream, float* us_out);
+
 /* out[t][i] = bf16(x[t][i] + sum_s part[s][t][i]) */
 mg_status mgd_residual(const uint16_t* x, const float* part, int32_t splits, int32_t T, int32_t N, uint16_t* out,
                        void* stream);

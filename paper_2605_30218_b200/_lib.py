@@ -59,7 +59,7 @@ DEBUG_SYMBOLS = ["mgd_gen_tensor", "mgd_rmsnorm", "mgd_gemm", "mgd_qkv_epilogue"
                  "mgd_attention_streams", "mgd_residual", "mgd_swiglu", "mgd_top2", "mgd_gate", "mgd_read_column", "mgd_cache_digest", "mgd_last_step",
                  "mgd_capture_logits", "mgd_weight", "mgd_schedule", "mgd_launch_count", "mgd_set_timing",
                  "mgd_timing", "mgd_capture_verifier_logits", "mgd_set_inject",
-                 "mgd_force_schedule", "mgd_gemm_top2"]
+                 "mgd_force_schedule", "mgd_gemm_top2", "mgd_launch_floor"]
 
 _vp, _i32, _u32, _i64, _u64, _f32 = C.c_void_p, C.c_int32, C.c_uint32, C.c_int64, C.c_uint64, C.c_float
 _P = C.POINTER
@@ -84,6 +84,7 @@ _SIGS = {
     "mgd_qkv_epilogue": [_vp, _i32, _vp, _vp, _i32, _i32, _i32, _i32, _f32, _i32, _vp, _vp, _vp, _vp],
     "mgd_attention": [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp],
     "mgd_attention_streams": [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp],
+    "mgd_launch_floor": [_i32, _i32, _vp, _vp],
     "mgd_residual": [_vp, _vp, _i32, _i32, _i32, _vp, _vp],
     "mgd_swiglu": [_vp, _i32, _i32, _i32, _vp, _vp],
     "mgd_top2": [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

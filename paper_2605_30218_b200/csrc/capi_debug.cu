@@ -13,6 +13,14 @@ using namespace mg;
 
 static mg_status st_of(cudaError_t e) { return e == cudaSuccess ? MG_OK : MG_ERR_CUDA; }
 
+// ---------------------------------------------------------------- launch floor
+namespace {
+__global__ void k_null() {
+  extern __shared__ unsigned char s_null[];
+  if (threadIdx.x == 1023) s_null[0] = 0;  // never true: keeps the shared-memory reservation
+}
+}  // namespace
+
 extern "C" {
 
 mg_status mgd_gen_tensor(uint64_t seed, uint32_t tid, int64_t n, int32_t kind, int32_t fan_in, uint16_t* out,
@@ -117,6 +125,31 @@ mg_status mgd_qkv_epilogue(const float* part, int32_t splits, const uint16_t* bi
   cudaFree(dc);
   cudaFree(ds);
   return st_of(e);
+}
+
+mg_status mgd_launch_floor(int32_t smem_bytes, int32_t reps, void* stream, float* us_out) {
+  if (!us_out || reps < 1 || smem_bytes < 0 || smem_bytes > 227 * 1024) return MG_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaFuncSetAttribute(k_null, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess)
+    return MG_ERR_CUDA;
+  cudaEvent_t a, b;
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return MG_ERR_CUDA;
+  const int grid = num_sms();
+  for (int i = 0; i < 5; ++i) k_null<<<grid, 192, smem_bytes, st>>>();
+  double sum = 0.0;
+  for (int i = 0; i < reps; ++i) {
+    cudaEventRecord(a, st);
+    k_null<<<grid, 192, smem_bytes, st>>>();
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    sum += ms;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *us_out = (float)(1e3 * sum / reps);
+  return st_of(cudaGetLastError());
 }
 
 mg_status mgd_attention(const uint16_t* q, const uint16_t* K, const uint16_t* V, const int32_t* n_keys, int32_t T,

@@ -1,0 +1,49 @@
+// launch_floor.cu -- the floor of an event-bracketed kernel launch on B200
+// (diagnostic only): an empty kernel with the GEMM's launch shape (148 CTAs x
+// 192 threads, 193 KB dynamic shared memory), the same without shared memory,
+// and a 1-CTA kernel; each timed (a) bracketed alone by two CUDA events, as
+// bench.py's per-launch roofline pass does, and (b) 100 back to back.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/launch_floor scripts/launch_floor.cu
+#include <cstdio>
+
+#include <cuda_runtime.h>
+
+__global__ void k_empty() {
+  extern __shared__ unsigned char s[];
+  if (threadIdx.x == 1023) s[0] = 0;  // never true: keeps the shared-memory reservation
+}
+
+static void run(const char* name, int grid, int block, int smem) {
+  cudaFuncSetAttribute(k_empty, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int i = 0; i < 10; ++i) k_empty<<<grid, block, smem>>>();
+  cudaDeviceSynchronize();
+  float iso = 0.f;
+  for (int i = 0; i < 100; ++i) {
+    cudaEventRecord(a);
+    k_empty<<<grid, block, smem>>>();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    iso += ms;
+  }
+  cudaEventRecord(a);
+  for (int i = 0; i < 100; ++i) k_empty<<<grid, block, smem>>>();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float btb;
+  cudaEventElapsedTime(&btb, a, b);
+  printf("%-40s isolated %6.2f us   back-to-back %6.2f us  (%s)\n", name, iso * 10.f, btb * 10.f,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  run("148 x 192, 193 KB smem (GEMM shape)", 148, 192, 193 * 1024);
+  run("148 x 192, no smem", 148, 192, 0);
+  run("512 x 128, 38 KB smem (attention shape)", 512, 128, 38 * 1024);
+  run("1 x 32", 1, 32, 0);
+  return 0;
+}
