@@ -2,7 +2,9 @@
 // (diagnostic only): an empty kernel with the GEMM's launch shape (148 CTAs x
 // 192 threads, 193 KB dynamic shared memory), the same without shared memory,
 // and a 1-CTA kernel; each timed (a) bracketed alone by two CUDA events, as
-// bench.py's per-launch roofline pass does, and (b) 100 back to back.
+// bench.py's per-launch roofline pass does, (b) 100 back to back, (c) 100
+// back to back with programmatic dependent launch (the kernel triggers its
+// dependents first, then waits), (d) the PDL chain of (c) as one CUDA graph.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/launch_floor scripts/launch_floor.cu
 #include <cstdio>
 
@@ -11,6 +13,27 @@
 __global__ void k_empty() {
   extern __shared__ unsigned char s[];
   if (threadIdx.x == 1023) s[0] = 0;  // never true: keeps the shared-memory reservation
+}
+
+__global__ void k_empty_pdl() {
+  extern __shared__ unsigned char s[];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 1023) s[0] = 0;
+}
+
+static void launch_pdl(int grid, int block, int smem, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_empty_pdl);
 }
 
 static void run(const char* name, int grid, int block, int smem) {
@@ -36,8 +59,33 @@ static void run(const char* name, int grid, int block, int smem) {
   cudaEventSynchronize(b);
   float btb;
   cudaEventElapsedTime(&btb, a, b);
-  printf("%-40s isolated %6.2f us   back-to-back %6.2f us  (%s)\n", name, iso * 10.f, btb * 10.f,
-         cudaGetErrorString(cudaGetLastError()));
+  cudaFuncSetAttribute(k_empty_pdl, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  for (int i = 0; i < 10; ++i) launch_pdl(grid, block, smem, st);
+  cudaStreamSynchronize(st);
+  cudaEventRecord(a, st);
+  for (int i = 0; i < 100; ++i) launch_pdl(grid, block, smem, st);
+  cudaEventRecord(b, st);
+  cudaEventSynchronize(b);
+  float pdl;
+  cudaEventElapsedTime(&pdl, a, b);
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  for (int i = 0; i < 100; ++i) launch_pdl(grid, block, smem, st);
+  cudaStreamEndCapture(st, &g);
+  cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphLaunch(ge, st);
+  cudaStreamSynchronize(st);
+  cudaEventRecord(a, st);
+  cudaGraphLaunch(ge, st);
+  cudaEventRecord(b, st);
+  cudaEventSynchronize(b);
+  float gr;
+  cudaEventElapsedTime(&gr, a, b);
+  printf("%-40s isolated %6.2f us   back-to-back %6.2f us   PDL %6.2f us   PDL graph %6.2f us  (%s)\n", name,
+         iso * 10.f, btb * 10.f, pdl * 10.f, gr * 10.f, cudaGetErrorString(cudaGetLastError()));
 }
 
 int main() {
