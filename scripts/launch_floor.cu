@@ -4,7 +4,9 @@
 // and a 1-CTA kernel; each timed (a) bracketed alone by two CUDA events, as
 // bench.py's per-launch roofline pass does, (b) 100 back to back, (c) 100
 // back to back with programmatic dependent launch (the kernel triggers its
-// dependents first, then waits), (d) the PDL chain of (c) as one CUDA graph.
+// dependents first, then waits), (d) the PDL chain of (c) as one CUDA graph;
+// and a graph chain of kernels that each spin 5 us with the dependent launch
+// triggered at the start vs at the end (what an early trigger buys).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/launch_floor scripts/launch_floor.cu
 #include <cstdio>
 
@@ -88,7 +90,60 @@ static void run(const char* name, int grid, int block, int smem) {
          iso * 10.f, btb * 10.f, pdl * 10.f, gr * 10.f, cudaGetErrorString(cudaGetLastError()));
 }
 
+__global__ void k_spin(long long ns, int trig_first) {
+  extern __shared__ unsigned char s[];
+  if (trig_first) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  long long t = t0;
+  while (t - t0 < ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (!trig_first) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x == 1023) s[0] = 0;
+}
+
+static void spin_chain(int smem, int trig_first) {
+  cudaFuncSetAttribute(k_spin, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  for (int i = 0; i < 100; ++i) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = 148;
+    cfg.blockDim = 192;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_spin, 5000LL, trig_first);
+  }
+  cudaStreamEndCapture(st, &g);
+  cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphLaunch(ge, st);
+  cudaStreamSynchronize(st);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, st);
+  cudaGraphLaunch(ge, st);
+  cudaEventRecord(b, st);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  printf("graph chain of 5 us spins, 148 x 192, %3d KB smem, trigger at %s: %6.2f us per kernel (%s)\n", smem / 1024,
+         trig_first ? "start" : "end  ", ms * 10.f, cudaGetErrorString(cudaGetLastError()));
+}
+
 int main() {
+  spin_chain(193 * 1024, 1);
+  spin_chain(193 * 1024, 0);
+  spin_chain(0, 1);
+  spin_chain(0, 0);
   run("148 x 192, 193 KB smem (GEMM shape)", 148, 192, 193 * 1024);
   run("148 x 192, no smem", 148, 192, 0);
   run("512 x 128, 38 KB smem (attention shape)", 512, 128, 38 * 1024);
