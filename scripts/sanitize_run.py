@@ -5,7 +5,10 @@ usage: compute-sanitizer --tool memcheck python scripts/sanitize_run.py
 Runs: prefill of 4 ragged prompts; 8 synchronous steps at tau = 0.3 with real
 triggers (the whole-step CUDA graph with conditional nodes from the second
 step on), then at tau = inf; 6 fused and 6 pipelined steps; a window verify;
-multi-split attention (verify_chunk 16, contexts > 64 keys)."""
+multi-split attention (verify_chunk 16, contexts > 64 keys); the small-grid
+(4, 4) attention rings (these grids have < 1 CTA per SM); and the fast path's
+2-stream attention CTAs through mgd_attention_streams (hd 128 and 64, one
+and several splits)."""
 import os
 import sys
 
@@ -33,4 +36,16 @@ for mode in (0, 2, 1):
     torch.cuda.synchronize()
     print("mode", mode, st)
     eng.close()
+import numpy as np  # noqa: E402
+
+from paper_2605_30218_b200 import kernels as K  # noqa: E402
+
+rng = np.random.default_rng(5)
+for H, KVh, hd, sk, nk in ((32, 8, 128, 512, (1, 37, 700)), (4, 4, 64, 64, (5, 130, 300))):
+    T, stride = len(nk), max(nk)
+    kv = rng.standard_normal((T, KVh, stride, hd)).astype(np.float32)
+    k16 = (kv.view(np.uint32) >> 16).astype(np.uint16)
+    q16 = (rng.standard_normal((T, H, hd)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    K.attention(q16, k16, k16, np.array(nk, np.int32), sk, streams=2)
+torch.cuda.synchronize()
 print("SANITIZE RUN OK")
