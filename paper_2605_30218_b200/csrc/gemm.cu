@@ -40,6 +40,9 @@
 #ifndef MG_EPI_STORE
 #define MG_EPI_STORE 1  // 1: partials via a shared-memory transpose and float4 stores; 0: scalar stores
 #endif
+#ifndef MG_PART_EVICT_LAST
+#define MG_PART_EVICT_LAST 1  // fp32 partial stores with an L2 evict_last hint
+#endif
 #ifndef MG_EPI_WAIT
 #define MG_EPI_WAIT mbar_wait  // accumulator-ready wait of the epilogue poller
 #endif
@@ -174,6 +177,9 @@ __global__ void __launch_bounds__(192, 1)
     __shared__ __align__(16) float s_val[4][16 * 33];  // per-warp [token][row] transposes (top-2 padded; stores dense)
     griddep_wait();
     const int q = warp & 3;
+#if MG_PART_EVICT_LAST
+    const uint64_t pol_part = policy_evict_last();
+#endif
     int j = 0;
     PieceIter pi(g, KB);
     for (; pi.next(pc); ++j) {
@@ -240,8 +246,15 @@ __global__ void __launch_bounds__(192, 1)
           for (int k = 0; k < 4; ++k) {
             const int idx = k * 32 + lane, i = idx >> 3, p4 = (idx & 7) * 4;
             const int t = t0 + c0 + i;
-            if (t < g.T)
+            if (t < g.T) {
+#if MG_PART_EVICT_LAST
+              // the partials are re-read from L2 by the next kernel: keep them
+              // there while the weight stream (evict_first) flows past
+              st_v4_hint(o + (size_t)t * g.N + n0 + p4, *reinterpret_cast<const float4*>(sv + i * 32 + p4), pol_part);
+#else
               *reinterpret_cast<float4*>(o + (size_t)t * g.N + n0 + p4) = *reinterpret_cast<const float4*>(sv + i * 32 + p4);
+#endif
+            }
           }
           __syncwarp();
 #else
