@@ -31,8 +31,11 @@ pytestmark = pytest.mark.gpu
 TOL = 2e-2
 INF = float("inf")
 
-# shape -> (batch, prompt length, decode steps, sampled row)
-CASES = {"llama8b": (64, 12, 3, 37), "qwen14b": (8, 10, 2, 5), "dsr1_7b": (8, 10, 2, 3)}
+# shape -> (batch, prompt length, decode steps, sampled row); "llama8b@128" is
+# configs[4]'s per-GPU batch: the 128-token GEMM tile and the fast path's
+# 2-stream attention CTAs (1024 > one wave of 4-warp CTAs)
+CASES = {"llama8b": (64, 12, 3, 37), "llama8b@128": (128, 12, 3, 101), "qwen14b": (8, 10, 2, 5),
+         "dsr1_7b": (8, 10, 2, 3)}
 
 
 def _host_ram_ok(shp):
@@ -59,12 +62,12 @@ def test_full_size_sampled_row_parity(orc, name):
     import torch
 
     from paper_2605_30218_b200.engine import Engine
-    shp = inputs.shape(name)
+    shp = inputs.shape(name.split("@")[0])
     if not _host_ram_ok(shp):
         pytest.skip("not enough host RAM for the oracle's weights")
     B, plen, steps, row = CASES[name]
     V = shp["vocab"]
-    max_seq = _bench_max_seq() if name == "llama8b" else 64
+    max_seq = _bench_max_seq() if name.startswith("llama8b") else 64
     prompts = inputs.prompts(B, plen, V, seed=4242)
     eng = Engine(shp, max_batch=B, max_slots=B, max_seq=max_seq, page_size=64)
     capf = torch.empty((B, V), dtype=torch.float32, device="cuda")
