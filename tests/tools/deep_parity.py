@@ -12,7 +12,7 @@ max(2e-2, 2 x the pooled |A - D| spread), tokens exactly
 outside the PAPER.md:203 band.  The oracle needs ~30 minutes of 16-core CPU
 time per plan at this depth, so this runs outside the pytest suite.
 
-usage: python scripts/deep_parity.py [steps] > profiles/r02_deep_parity_llama8b.json
+usage: python tests/tools/deep_parity.py [steps] > profiles/r02_deep_parity_llama8b.json
 """
 import json
 import os
@@ -22,7 +22,7 @@ import time
 import numpy as np
 import torch
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import oracle as orc  # noqa: E402
 from paper_2605_30218_b200 import inputs  # noqa: E402

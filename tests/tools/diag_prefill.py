@@ -3,7 +3,7 @@ columns, GPU vs oracle (tiny config)."""
 import os, sys
 import numpy as np
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import oracle
 from paper_2605_30218_b200 import inputs
 from paper_2605_30218_b200.engine import Engine
